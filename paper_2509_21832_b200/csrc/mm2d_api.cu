@@ -1,0 +1,764 @@
+// C ABI of libmm2d.so (declared in include/mm2d.h).  Owns the per-problem
+// context: device buffers, launch configuration, CUDA graphs and the sticky
+// error word.  See mm2d.h for the reference interfaces each entry replaces.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mm2d.h"
+#include "mm2d_common.cuh"
+#include "mm2d_contract.cuh"
+#include "mm2d_macro.cuh"
+#include "mm2d_micro.cuh"
+#include "mm2d_prep.cuh"
+
+using namespace mm2d;
+
+static std::atomic<long long> g_launches{0};
+
+struct mm2d_ctx {
+    mm2d_config cfg;
+    Geometry g;
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    double* d_v1 = nullptr;
+    double* d_v2 = nullptr;
+    CellPar* d_P = nullptr;
+    double* d_Qr = nullptr;
+    double* d_Hr = nullptr;
+    double* d_Qx = nullptr;
+    unsigned long long* d_err = nullptr;   // [0] key, [1..4] iso maxima
+    // halo buffers for the micro field (multi-rank only)
+    double* d_gh[4] = {nullptr, nullptr, nullptr, nullptr};
+    // context-owned state
+    double* d_Qs[2] = {nullptr, nullptr};
+    double* d_Gs[2] = {nullptr, nullptr};
+    double* d_Hsoa = nullptr;
+    int cur = 0;
+    // micro launch configuration
+    int BX = 2, NE = 4, NT = 256, ly = 32;
+    bool fast = true;
+    size_t smem = 0;
+    const void* micro_fn = nullptr;
+    // graphs for context-owned stepping (parity 0: A->B, 1: B->A)
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    double graph_dt = 0.0;
+    double last_dt = 0.0;
+    double* last_Qout = nullptr;
+    bool counting = true;
+    long long launches_per_step = 7;
+    bool state_owned = false;
+    cudaStream_t user_stream = nullptr;
+    bool have_user_stream = false;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    std::string err;
+};
+
+#define CK(call)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            if (ctx) ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);    \
+            return MM2D_ERR_INTERNAL;                                                  \
+        }                                                                              \
+    } while (0)
+
+static int fail_cfg(mm2d_ctx* ctx, const std::string& m) {
+    if (ctx) ctx->err = m;
+    return MM2D_ERR_CONFIG;
+}
+
+// ---- micro kernel instantiations ----
+template <int NE, int BX, bool FAST>
+static const void* micro_ptr() {
+    return reinterpret_cast<const void*>(&k_micro<NE, BX, FAST>);
+}
+
+static const void* pick_micro(int NE, int BX, bool fast) {
+#define PICK(ne, bx)                                              \
+    if (NE == ne && BX == bx) return fast ? micro_ptr<ne, bx, true>() : micro_ptr<ne, bx, false>();
+    PICK(2, 1) PICK(2, 2) PICK(4, 1) PICK(4, 2) PICK(8, 1) PICK(8, 2)
+#undef PICK
+    return nullptr;
+}
+
+static int ghost_mode(const mm2d_config& c, int face, bool at_edge, int nranks_axis, int field) {
+    // field 0: micro G (walls zero), 1: macro Q (walls copy), 2: heat (walls zero)
+    if (!at_edge) return GM_HALO;
+    const int kind = c.face[face];
+    if (kind == MM2D_FACE_PERIODIC) return nranks_axis > 1 ? GM_HALO : GM_WRAP;
+    if (kind == MM2D_FACE_EXTRAPOLATE) return GM_COPY;
+    return field == 1 ? GM_COPY : GM_ZERO;
+}
+
+extern "C" int mm2d_version(void) { return 1; }
+
+extern "C" const char* mm2d_last_error(mm2d_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+extern "C" long long mm2d_launch_count(void) { return g_launches.load(); }
+extern "C" void mm2d_reset_launch_count(void) { g_launches.store(0); }
+
+extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
+    if (!cfg || !out) return MM2D_ERR_CONFIG;
+    *out = nullptr;
+    mm2d_ctx* ctx = new mm2d_ctx();
+    ctx->cfg = *cfg;
+    const mm2d_config& c = ctx->cfg;
+    if (c.nx < 1 || c.ny < 1 || c.nv1 < 2 || c.nv2 < 2) {
+        int r = fail_cfg(ctx, "grid sizes must be nx, ny >= 1 and nv1, nv2 >= 2");
+        delete ctx;
+        return r;
+    }
+    if (c.px < 1 || c.py < 1 || c.nx % c.px || c.ny % c.py || c.rx < 0 || c.rx >= c.px ||
+        c.ry < 0 || c.ry >= c.py) {
+        int r = fail_cfg(ctx, "rank grid must divide the spatial grid (make_plans)");
+        delete ctx;
+        return r;
+    }
+    for (int f = 0; f < 4; ++f)
+        if (c.face[f] < 0 || c.face[f] > 2) {
+            int r = fail_cfg(ctx, "unknown face kind");
+            delete ctx;
+            return r;
+        }
+    if ((c.face[0] == MM2D_FACE_PERIODIC) != (c.face[1] == MM2D_FACE_PERIODIC) ||
+        (c.face[2] == MM2D_FACE_PERIODIC) != (c.face[3] == MM2D_FACE_PERIODIC)) {
+        int r = fail_cfg(ctx, "periodic boundaries must come in pairs");
+        delete ctx;
+        return r;
+    }
+    if (!(c.nu >= -1.0 && c.nu < 1.0)) {
+        int r = fail_cfg(ctx, "nu must lie in [-1, 1)");
+        delete ctx;
+        return r;
+    }
+    ctx->dev = c.device;
+    if (cudaSetDevice(ctx->dev) != cudaSuccess) {
+        int r = fail_cfg(ctx, "cudaSetDevice failed");
+        delete ctx;
+        return r;
+    }
+    Geometry& g = ctx->g;
+    memset(&g, 0, sizeof(g));
+    g.nx = c.nx; g.ny = c.ny;
+    g.bx = c.nx / c.px; g.by = c.ny / c.py;
+    g.i0 = c.rx * g.bx; g.j0 = c.ry * g.by;
+    g.nv1 = c.nv1; g.nv2 = c.nv2; g.V = c.nv1 * c.nv2;
+    g.dx = (c.x_max - c.x_min) / c.nx;
+    g.dy = (c.y_max - c.y_min) / c.ny;
+    const bool e[4] = {c.rx == 0, c.rx == c.px - 1, c.ry == 0, c.ry == c.py - 1};
+    const int nr[4] = {c.px, c.px, c.py, c.py};
+    int* gm[3][4] = {{&g.xlo, &g.xhi, &g.ylo, &g.yhi},
+                     {&g.qxlo, &g.qxhi, &g.qylo, &g.qyhi},
+                     {&g.hxlo, &g.hxhi, &g.hylo, &g.hyhi}};
+    for (int fld = 0; fld < 3; ++fld)
+        for (int f = 0; f < 4; ++f) *gm[fld][f] = ghost_mode(c, f, e[f], nr[f], fld);
+    for (int f = 0; f < 4; ++f) {
+        g.phys[f] = e[f] && c.face[f] != MM2D_FACE_PERIODIC;
+        g.wall[f] = e[f] && c.face[f] == MM2D_FACE_WALL;
+        g.wallT[f] = c.wall_T[f];
+        g.wallU[f] = c.wall_U[f];
+        if (c.face[f] == MM2D_FACE_WALL && !(c.wall_T[f] > 0.0)) {
+            int r = fail_cfg(ctx, "wall temperature must be positive");
+            delete ctx;
+            return r;
+        }
+    }
+    // launch configuration of the fused micro kernel
+    const int V = g.V;
+    ctx->fast = (c.nv2 % 2) == 0;
+    int NE = 2;
+    if (ctx->fast) {
+        NE = V <= 512 ? 2 : V <= 1024 ? 4 : 8;
+    } else {
+        NE = V <= 1024 ? 4 : 8;
+    }
+    const int per = (V + NE - 1) / NE;
+    int NT = ((per + 31) / 32) * 32;
+    if (NT > 256) {
+        int r = fail_cfg(ctx, "velocity grid too large (nv1*nv2 <= 2048 supported)");
+        delete ctx;
+        return r;
+    }
+    ctx->NE = NE;
+    ctx->NT = NT;
+    ctx->BX = (g.bx >= 2 && V <= 1024) ? 2 : 1;
+    ctx->ly = std::min(g.by, 32);
+    ctx->micro_fn = pick_micro(NE, ctx->BX, ctx->fast);
+    ctx->smem = micro_smem_bytes(ctx->BX, V, c.nv1, c.nv2);
+    if (!ctx->micro_fn) {
+        int r = fail_cfg(ctx, "no micro kernel instantiation for this velocity grid");
+        delete ctx;
+        return r;
+    }
+    if (cudaFuncSetAttribute(ctx->micro_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ctx->smem) != cudaSuccess) {
+        int r = fail_cfg(ctx, "shared memory request too large for the micro kernel");
+        delete ctx;
+        return r;
+    }
+    // buffers
+    const size_t ring = (size_t)(g.bx + 2) * (g.by + 2);
+    std::vector<double> v1(c.nv1), v2(c.nv2);
+    const double h1 = (c.v1_max - c.v1_min) / c.nv1, h2 = (c.v2_max - c.v2_min) / c.nv2;
+    for (int k = 0; k < c.nv1; ++k) v1[k] = c.v1_min + ((k + 1) - 0.5) * h1;
+    for (int l = 0; l < c.nv2; ++l) v2[l] = c.v2_min + ((l + 1) - 0.5) * h2;
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&ctx->d_v1, sizeof(double) * c.nv1));
+    CK(cudaMalloc(&ctx->d_v2, sizeof(double) * c.nv2));
+    CK(cudaMemcpy(ctx->d_v1, v1.data(), sizeof(double) * c.nv1, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_v2, v2.data(), sizeof(double) * c.nv2, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&ctx->d_P, sizeof(CellPar) * ring));
+    CK(cudaMalloc(&ctx->d_Qr, sizeof(double) * 6 * ring));
+    CK(cudaMalloc(&ctx->d_Hr, sizeof(double) * 4 * ring));
+    CK(cudaMalloc(&ctx->d_Qx, sizeof(double) * 6 * ring));
+    CK(cudaMemset(ctx->d_Qr, 0, sizeof(double) * 6 * ring));
+    CK(cudaMemset(ctx->d_Hr, 0, sizeof(double) * 4 * ring));
+    CK(cudaMemset(ctx->d_Qx, 0, sizeof(double) * 6 * ring));
+    CK(cudaMalloc(&ctx->d_err, sizeof(unsigned long long) * 8));
+    {
+        unsigned long long init[8] = {kNoError, 0, 0, 0, 0, 0, 0, 0};
+        CK(cudaMemcpy(ctx->d_err, init, sizeof(init), cudaMemcpyHostToDevice));
+    }
+    const size_t Vs = (size_t)V;
+    for (int f = 0; f < 4; ++f) {
+        const bool halo = *gm[0][f] == GM_HALO;
+        if (!halo) continue;
+        const size_t cells = f < 2 ? (size_t)g.by : (size_t)g.bx + 2;
+        CK(cudaMalloc(&ctx->d_gh[f], sizeof(double) * cells * Vs));
+        CK(cudaMemset(ctx->d_gh[f], 0, sizeof(double) * cells * Vs));
+    }
+    *out = ctx;
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_destroy(mm2d_ctx* ctx) {
+    if (!ctx) return MM2D_OK;
+    cudaSetDevice(ctx->dev);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (int p = 0; p < 2; ++p) {
+        if (ctx->gexec[p]) cudaGraphExecDestroy(ctx->gexec[p]);
+        if (ctx->state_owned) {
+            cudaFree(ctx->d_Qs[p]);
+            cudaFree(ctx->d_Gs[p]);
+        }
+    }
+    if (ctx->state_owned) cudaFree(ctx->d_Hsoa);
+    if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+    if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+    for (int f = 0; f < 4; ++f) cudaFree(ctx->d_gh[f]);
+    cudaFree(ctx->d_v1); cudaFree(ctx->d_v2); cudaFree(ctx->d_P); cudaFree(ctx->d_Qr);
+    cudaFree(ctx->d_Hr); cudaFree(ctx->d_Qx); cudaFree(ctx->d_err);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_block(mm2d_ctx* ctx, int* bx, int* by, int* i0, int* j0) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    if (bx) *bx = ctx->g.bx;
+    if (by) *by = ctx->g.by;
+    if (i0) *i0 = ctx->g.i0;
+    if (j0) *j0 = ctx->g.j0;
+    return MM2D_OK;
+}
+
+// (4, bx, by) SoA heat tensor from the ring
+__global__ void k_h_soa(Geometry g, const double* Hr, double* H) {
+    const int n = g.bx * g.by;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = t / g.by, j = t % g.by;
+        const double* h = Hr + 4 * ring_index(g, i, j);
+        for (int c = 0; c < 4; ++c) H[(size_t)c * n + t] = h[c];
+    }
+}
+
+static int grid_for(long long n, int threads) {
+    long long b = (n + threads - 1) / threads;
+    return (int)std::max(1LL, std::min(b, 148LL * 32));
+}
+
+// enqueue one full step on `s` (graph-capturable: no host syncs)
+static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double dt, double* Qout,
+                        double* Gout, double* H, int nsrc, const double* sc, const double* ss,
+                        const double* qsrc, cudaStream_t s, cudaEvent_t* ev = nullptr) {
+#define MARK(q) \
+    if (ev) CK(cudaEventRecord(ev[q], s))
+    const Geometry& g = ctx->g;
+    const mm2d_config& c = ctx->cfg;
+    const long long ring = (long long)(g.bx + 2) * (g.by + 2);
+    const bool gauss = c.nu != 0.0;
+    // isotropy maxima for the eps < 1e-10 guard (micro2d.py:96)
+    long long nl = 0;
+    if (gauss && c.eps < 1e-10) {
+        CK(cudaMemsetAsync(ctx->d_err + 1, 0, sizeof(unsigned long long) * 4, s));
+    }
+    ctx->last_dt = dt;
+    ctx->last_Qout = Qout;
+    MARK(0);
+    k_fill_qring<<<grid_for(ring, 256), 256, 0, s>>>(g, Q, ctx->d_Qr, ctx->d_err);
+    MARK(1);
+    PrepArgs pa;
+    pa.g = g; pa.Qr = ctx->d_Qr; pa.P = ctx->d_P; pa.err = ctx->d_err; pa.iso = ctx->d_err + 1;
+    pa.dt = dt; pa.eps = c.eps; pa.nu = c.nu;
+    {
+        const double h1 = (c.v1_max - c.v1_min) / c.nv1, h2 = (c.v2_max - c.v2_min) / c.nv2;
+        const double v10 = c.v1_min + 0.5 * h1, v11 = c.v1_min + 1.5 * h1;
+        const double v20 = c.v2_min + 0.5 * h2, v21 = c.v2_min + 1.5 * h2;
+        pa.dv = (v11 - v10) * (v21 - v20);
+    }
+    pa.tau_kind = c.tau_kind; pa.tau_value = c.tau_value;
+    pa.step = 0;
+    pa.gauss = gauss;
+    k_prep<<<grid_for(ring, 128), 128, 0, s>>>(pa);
+    MARK(2);
+    MicroArgs ma;
+    memset(&ma, 0, sizeof(ma));
+    ma.g = g; ma.G = G; ma.Gout = Gout;
+    ma.hxlo = ctx->d_gh[0]; ma.hxhi = ctx->d_gh[1]; ma.hylo = ctx->d_gh[2]; ma.hyhi = ctx->d_gh[3];
+    ma.P = ctx->d_P; ma.Hr = ctx->d_Hr; ma.v1 = ctx->d_v1; ma.v2 = ctx->d_v2;
+    ma.err = ctx->d_err; ma.iso = ctx->d_err + 1;
+    ma.src_coeffs = sc; ma.src_shapes = ss; ma.nsrc = nsrc;
+    ma.ly = ctx->ly; ma.gauss = gauss;
+    ma.dt = dt; ma.eps = c.eps; ma.inveps = 1.0 / c.eps;
+    ma.idx = 1.0 / g.dx; ma.idy = 1.0 / g.dy;
+    ma.dv = pa.dv; ma.hfac = c.eps * pa.dv;
+    {
+        dim3 grid((g.bx + ctx->BX - 1) / ctx->BX, (g.by + ctx->ly - 1) / ctx->ly);
+        void* args[] = {&ma};
+        CK(cudaLaunchKernel(ctx->micro_fn, grid, dim3(ctx->NT), args, ctx->smem, s));
+    }
+    MARK(3);
+    k_fill_hring<<<grid_for(ring, 256), 256, 0, s>>>(g, ctx->d_Hr);
+    MARK(4);
+    MacroArgs mc;
+    mc.g = g; mc.Qr = ctx->d_Qr; mc.Hr = ctx->d_Hr; mc.Qx = ctx->d_Qx; mc.Qout = Qout;
+    mc.qsrc = qsrc; mc.err = ctx->d_err; mc.dt = dt; mc.eps = c.eps; mc.nu = c.nu;
+    mc.rx = dt / g.dx; mc.ry = dt / g.dy; mc.tau_kind = c.tau_kind; mc.tau_value = c.tau_value;
+    mc.step = 0;
+    k_macro_x<<<grid_for((long long)g.bx * (g.by + 2), 128), 128, 0, s>>>(mc);
+    MARK(5);
+    k_macro_y<<<grid_for((long long)g.bx * g.by, 128), 128, 0, s>>>(mc);
+    MARK(6);
+    nl += 6;
+    if (H) {
+        k_h_soa<<<grid_for((long long)g.bx * g.by, 256), 256, 0, s>>>(g, ctx->d_Hr, H);
+        ++nl;
+    }
+    MARK(7);
+#undef MARK
+    CK(cudaGetLastError());
+    ctx->launches_per_step = nl;
+    if (ctx->counting) g_launches += nl;
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_step(mm2d_ctx* ctx, const double* d_Q, const double* d_G, double dt,
+                         double* d_Qout, double* d_Gout, double* d_H, int nsrc,
+                         const double* d_src_coeffs, const double* d_src_shapes,
+                         const double* d_qsrc, void* stream) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t s = (cudaStream_t)stream;   // 0 = the legacy default stream
+    return enqueue_step(ctx, d_Q, d_G, dt, d_Qout, d_Gout, d_H, nsrc, d_src_coeffs,
+                        d_src_shapes, d_qsrc, s);
+}
+
+static void drop_graphs(mm2d_ctx* ctx) {
+    for (int p = 0; p < 2; ++p)
+        if (ctx->gexec[p]) { cudaGraphExecDestroy(ctx->gexec[p]); ctx->gexec[p] = nullptr; }
+}
+
+extern "C" int mm2d_alloc_state(mm2d_ctx* ctx) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    CK(cudaSetDevice(ctx->dev));
+    if (!ctx->state_owned) {
+        drop_graphs(ctx);
+        for (int p = 0; p < 2; ++p) ctx->d_Qs[p] = ctx->d_Gs[p] = nullptr;
+        ctx->d_Hsoa = nullptr;
+        ctx->state_owned = true;
+    }
+    const size_t cells = (size_t)ctx->g.bx * ctx->g.by;
+    for (int p = 0; p < 2; ++p) {
+        if (!ctx->d_Qs[p]) CK(cudaMalloc(&ctx->d_Qs[p], sizeof(double) * 6 * cells));
+        if (!ctx->d_Gs[p]) CK(cudaMalloc(&ctx->d_Gs[p], sizeof(double) * cells * ctx->g.V));
+    }
+    if (!ctx->d_Hsoa) CK(cudaMalloc(&ctx->d_Hsoa, sizeof(double) * 4 * cells));
+    ctx->cur = 0;
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_attach_state(mm2d_ctx* ctx, double* d_Qa, double* d_Ga, double* d_Qb,
+                                 double* d_Gb, double* d_H) {
+    if (!ctx || !d_Qa || !d_Ga || !d_Qb || !d_Gb) return fail_cfg(ctx, "attach needs 4 buffers");
+    CK(cudaSetDevice(ctx->dev));
+    if (ctx->state_owned) {
+        for (int p = 0; p < 2; ++p) { cudaFree(ctx->d_Qs[p]); cudaFree(ctx->d_Gs[p]); }
+        cudaFree(ctx->d_Hsoa);
+        ctx->state_owned = false;
+    }
+    const bool same = ctx->d_Qs[0] == d_Qa && ctx->d_Gs[0] == d_Ga && ctx->d_Qs[1] == d_Qb &&
+                      ctx->d_Gs[1] == d_Gb && ctx->d_Hsoa == d_H;
+    if (!same) drop_graphs(ctx);
+    ctx->d_Qs[0] = d_Qa; ctx->d_Gs[0] = d_Ga; ctx->d_Qs[1] = d_Qb; ctx->d_Gs[1] = d_Gb;
+    ctx->d_Hsoa = d_H;
+    ctx->cur = 0;
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_current_index(mm2d_ctx* ctx) { return ctx ? ctx->cur : -1; }
+
+extern "C" int mm2d_set_stream(mm2d_ctx* ctx, void* stream) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    CK(cudaSetDevice(ctx->dev));
+    ctx->user_stream = (cudaStream_t)stream;
+    ctx->have_user_stream = true;
+    if (!ctx->ev_in) CK(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+    if (!ctx->ev_out) CK(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_upload(mm2d_ctx* ctx, const double* h_Q, const double* h_G) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    int r = mm2d_alloc_state(ctx);
+    if (r) return r;
+    const size_t cells = (size_t)ctx->g.bx * ctx->g.by;
+    CK(cudaMemcpyAsync(ctx->d_Qs[ctx->cur], h_Q, sizeof(double) * 6 * cells,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_Gs[ctx->cur], h_G, sizeof(double) * cells * ctx->g.V,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_upload_device(mm2d_ctx* ctx, const double* d_Q, const double* d_G) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    int r = mm2d_alloc_state(ctx);
+    if (r) return r;
+    const size_t cells = (size_t)ctx->g.bx * ctx->g.by;
+    CK(cudaMemcpyAsync(ctx->d_Qs[ctx->cur], d_Q, sizeof(double) * 6 * cells,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_Gs[ctx->cur], d_G, sizeof(double) * cells * ctx->g.V,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_run(mm2d_ctx* ctx, double dt, int nsteps) {
+    if (!ctx || !ctx->d_Qs[0]) return fail_cfg(ctx, "mm2d_run needs context-owned state");
+    CK(cudaSetDevice(ctx->dev));
+    if (ctx->graph_dt != dt || !ctx->gexec[0]) {
+        drop_graphs(ctx);
+        for (int p = 0; p < 2; ++p) {
+            cudaGraph_t graph;
+            CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            ctx->counting = false;
+            int r = enqueue_step(ctx, ctx->d_Qs[p], ctx->d_Gs[p], dt, ctx->d_Qs[1 - p],
+                                 ctx->d_Gs[1 - p], ctx->d_Hsoa, 0, nullptr, nullptr, nullptr,
+                                 ctx->stream);
+            ctx->counting = true;
+            cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+            if (r) return r;
+            CK(e);
+            CK(cudaGraphInstantiate(&ctx->gexec[p], graph, 0));
+            cudaGraphDestroy(graph);
+        }
+        ctx->graph_dt = dt;
+    }
+    if (ctx->have_user_stream) {
+        CK(cudaEventRecord(ctx->ev_in, ctx->user_stream));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in, 0));
+    }
+    for (int n = 0; n < nsteps; ++n) {
+        CK(cudaGraphLaunch(ctx->gexec[ctx->cur], ctx->stream));
+        ctx->cur ^= 1;
+        g_launches += ctx->launches_per_step;
+    }
+    if (ctx->have_user_stream) {
+        CK(cudaEventRecord(ctx->ev_out, ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->user_stream, ctx->ev_out, 0));
+    }
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_time_kernels(mm2d_ctx* ctx, double dt, int nrep, double* ms) {
+    if (!ctx || !ctx->d_Qs[0] || !ms || nrep < 1) return fail_cfg(ctx, "time_kernels needs state");
+    CK(cudaSetDevice(ctx->dev));
+    cudaEvent_t ev[8];
+    for (int q = 0; q < 8; ++q) CK(cudaEventCreate(&ev[q]));
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    if (ctx->have_user_stream) {
+        CK(cudaEventRecord(ev[0], ctx->user_stream));
+        CK(cudaStreamWaitEvent(ctx->stream, ev[0], 0));
+    }
+    for (int r = 0; r < nrep; ++r) {
+        const int p = ctx->cur;
+        int rc = enqueue_step(ctx, ctx->d_Qs[p], ctx->d_Gs[p], dt, ctx->d_Qs[1 - p],
+                              ctx->d_Gs[1 - p], ctx->d_Hsoa, 0, nullptr, nullptr, nullptr,
+                              ctx->stream, ev);
+        if (rc) return rc;
+        ctx->cur ^= 1;
+        CK(cudaEventSynchronize(ev[7]));
+        for (int q = 0; q < 7; ++q) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, ev[q], ev[q + 1]));
+            acc[q] += t;
+        }
+    }
+    for (int q = 0; q < 7; ++q) ms[q] = acc[q] / nrep;
+    for (int q = 0; q < 8; ++q) cudaEventDestroy(ev[q]);
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_download(mm2d_ctx* ctx, double* h_Q, double* h_G, double* h_H) {
+    if (!ctx || !ctx->d_Qs[0]) return fail_cfg(ctx, "no context-owned state");
+    CK(cudaSetDevice(ctx->dev));
+    const size_t cells = (size_t)ctx->g.bx * ctx->g.by;
+    if (h_Q)
+        CK(cudaMemcpyAsync(h_Q, ctx->d_Qs[ctx->cur], sizeof(double) * 6 * cells,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_G)
+        CK(cudaMemcpyAsync(h_G, ctx->d_Gs[ctx->cur], sizeof(double) * cells * ctx->g.V,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    if (h_H)
+        CK(cudaMemcpyAsync(h_H, ctx->d_Hsoa, sizeof(double) * 4 * cells, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_state_ptrs(mm2d_ctx* ctx, double** d_Q, double** d_G, double** d_H) {
+    if (!ctx || !ctx->d_Qs[0]) return fail_cfg(ctx, "no context-owned state");
+    if (d_Q) *d_Q = ctx->d_Qs[ctx->cur];
+    if (d_G) *d_G = ctx->d_Gs[ctx->cur];
+    if (d_H) *d_H = ctx->d_Hsoa;
+    return MM2D_OK;
+}
+
+// frame-style heat tensor: u from the given Q (cases.py:167-176)
+__global__ void k_heat_frame(Geometry g, const double* G, const double* Q, const double* v1,
+                             const double* v2, double f, double* H) {
+    __shared__ double sh[32];
+    const size_t c = blockIdx.x, V = (size_t)g.V;
+    const double rho = Q[6 * c], u1 = Q[6 * c + 1] / rho, u2 = Q[6 * c + 2] / rho;
+    double s[4] = {0, 0, 0, 0};
+    for (int n = threadIdx.x; n < (int)V; n += blockDim.x) {
+        const int k = n / g.nv2, l = n % g.nv2;
+        const double w1 = v1[k] - u1, w2 = v2[l] - u2, gg = G[c * V + n];
+        s[0] += w1 * w1 * w1 * gg; s[1] += w1 * w1 * w2 * gg;
+        s[2] += w1 * w2 * w2 * gg; s[3] += w2 * w2 * w2 * gg;
+    }
+    const size_t S = (size_t)g.bx * g.by;
+    for (int q = 0; q < 4; ++q) {
+        const double t = block_sum(s[q], sh);
+        if (threadIdx.x == 0) H[q * S + c] = f * t;
+    }
+}
+
+extern "C" int mm2d_heat_tensor(mm2d_ctx* ctx, const double* d_G, const double* d_Q,
+                                double* d_H, void* stream) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    CK(cudaSetDevice(ctx->dev));
+    cudaStream_t s = (cudaStream_t)stream;   // 0 = the legacy default stream
+    const mm2d_config& c = ctx->cfg;
+    const double h1 = (c.v1_max - c.v1_min) / c.nv1, h2 = (c.v2_max - c.v2_min) / c.nv2;
+    const double dv = ((c.v1_min + 1.5 * h1) - (c.v1_min + 0.5 * h1)) *
+                      ((c.v2_min + 1.5 * h2) - (c.v2_min + 0.5 * h2));
+    k_heat_frame<<<ctx->g.bx * ctx->g.by, 256, 0, s>>>(ctx->g, d_G, d_Q, ctx->d_v1, ctx->d_v2,
+                                                       c.eps * dv, d_H);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_sync(mm2d_ctx* ctx) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaDeviceSynchronize());
+    return MM2D_OK;
+}
+
+// value of the failing check, recomputed from the preserved stage input
+__global__ void k_err_value(Geometry g, int stage, int i, int j, const double* Qr,
+                            const double* Qx, const double* Qout, double nu, int tau_kind, double tau_value,
+                            double dt, double eps, double* out) {
+    double q[6];
+    const double* src = (stage <= ES_MOD_SPD) ? Qr + 6 * ring_index(g, i, j)
+                        : (stage >= ES_RL_RHO) ? Qout + 6 * ((size_t)i * g.by + j)
+                                               : Qx + 6 * ring_index(g, i, j);
+    for (int m = 0; m < 6; ++m) q[m] = src[m];
+    if (stage == ES_XS_RHO || stage == ES_XS_SPD) {
+        MacroArgs a;
+        a.dt = dt; a.eps = eps; a.nu = nu; a.tau_kind = tau_kind; a.tau_value = tau_value;
+        double o[6];
+        relax_cell(a, q, o);
+        for (int m = 0; m < 6; ++m) q[m] = o[m];
+    }
+    double rho, u1, u2, t11, t12, t22;
+    rho = q[0];
+    if (stage == ES_PRIM_RHO || stage == ES_XS_RHO || stage == ES_YS_RHO || stage == ES_RL_RHO) {
+        *out = rho;
+        return;
+    }
+    prims_of(q, rho, u1, u2, t11, t12, t22);
+    if (stage == ES_MOD_SPD) {
+        const double T = 0.5 * (t11 + t22);
+        const double m11 = (1.0 - nu) * T + nu * t11, m12 = nu * t12, m22 = (1.0 - nu) * T + nu * t22;
+        *out = m11 * m22 - m12 * m12;
+        return;
+    }
+    *out = t11 * t22 - t12 * t12;
+}
+
+extern "C" int mm2d_check(mm2d_ctx* ctx, int* kind, int* i, int* j, double* value) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaDeviceSynchronize());
+    unsigned long long key;
+    CK(cudaMemcpy(&key, ctx->d_err, sizeof(key), cudaMemcpyDeviceToHost));
+    if (key == kNoError) return MM2D_OK;
+    const int stage = (int)((key >> 36) & 0xf);
+    const unsigned long long cell = key & ((1ull << 36) - 1);
+    const int gi = (int)(cell / ctx->g.ny), gj = (int)(cell % ctx->g.ny);
+    const int li = gi - ctx->g.i0, lj = gj - ctx->g.j0;
+    int k = MM2D_STATE_PRESSURE;
+    if (stage == ES_PRIM_RHO || stage == ES_XS_RHO || stage == ES_YS_RHO || stage == ES_RL_RHO)
+        k = MM2D_STATE_DENSITY;
+    else if (stage == ES_MOD_SPD)
+        k = MM2D_STATE_MODIFIED;
+    double* d_v;
+    double v = 0.0;
+    CK(cudaMalloc(&d_v, sizeof(double)));
+    const mm2d_config& c = ctx->cfg;
+    k_err_value<<<1, 1>>>(ctx->g, stage, li, lj, ctx->d_Qr, ctx->d_Qx, ctx->last_Qout, c.nu,
+                          c.tau_kind, c.tau_value, ctx->last_dt, c.eps, d_v);
+    CK(cudaMemcpy(&v, d_v, sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(d_v);
+    if (kind) *kind = k;
+    if (i) *i = gi;
+    if (j) *j = gj;
+    if (value) *value = v;
+    char buf[160];
+    snprintf(buf, sizeof buf, "invalid state (stage %d) at cell (%d, %d)", stage, gi, gj);
+    ctx->err = buf;
+    return MM2D_ERR_STATE;
+}
+
+extern "C" int mm2d_halo_info(mm2d_ctx* ctx, int which, int slot, double** d_send,
+                              double** d_recv, long long* count) {
+    (void)which; (void)slot; (void)d_send; (void)d_recv; (void)count;
+    return fail_cfg(ctx, "halo exchange buffers are not enabled in this build");
+}
+extern "C" int mm2d_halo_pack(mm2d_ctx* ctx, int which, const double* d_src, void* stream) {
+    (void)which; (void)d_src; (void)stream;
+    return fail_cfg(ctx, "halo exchange buffers are not enabled in this build");
+}
+extern "C" int mm2d_halo_unpack(mm2d_ctx* ctx, int which, void* stream) {
+    (void)which; (void)stream;
+    return fail_cfg(ctx, "halo exchange buffers are not enabled in this build");
+}
+
+// ---------------------------------------------------------------------------
+// the ten kernel-contract entry points
+// ---------------------------------------------------------------------------
+#define KCK()                                                         \
+    do {                                                              \
+        cudaError_t e_ = cudaGetLastError();                          \
+        if (e_ != cudaSuccess) return MM2D_ERR_INTERNAL;              \
+        g_launches += 1;                                              \
+        return MM2D_OK;                                               \
+    } while (0)
+
+static int nblk(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 64); }
+
+extern "C" int mm2d_k_maxwellian_field_2d(int nx, int ny, int nv1, int nv2, const double* rho,
+                                          const double* u1, const double* u2, const double* T,
+                                          const double* v1, const double* v2, double* M,
+                                          void* stream) {
+    kc_maxwellian<<<nblk((size_t)nx * ny * nv1 * nv2), 256, 0, (cudaStream_t)stream>>>(
+        nx * ny, nv1, nv2, rho, u1, u2, T, v1, v2, M);
+    KCK();
+}
+
+extern "C" int mm2d_k_project_field_2d(int nx, int ny, int nv1, int nv2, const double* F,
+                                       const double* M, const double* rho, const double* u1,
+                                       const double* u2, const double* T, const double* v1,
+                                       const double* v2, double dv, double* out, void* stream) {
+    kc_project<<<nx * ny, 128, 0, (cudaStream_t)stream>>>(nv1, nv2, F, M, rho, u1, u2, T, v1, v2,
+                                                          dv, out);
+    KCK();
+}
+
+extern "C" int mm2d_k_transport_stage_2d(int nx, int ny, int nv1, int nv2, const double* G_ext,
+                                         const double* M, const double* rho, const double* u1,
+                                         const double* u2, const double* T, const double* v1,
+                                         const double* v2, double d, double dt, int axis,
+                                         double* out, void* stream) {
+    kc_transport<<<nx * ny, 128, 0, (cudaStream_t)stream>>>(nx, ny, nv1, nv2, G_ext, M, rho, u1,
+                                                            u2, T, v1, v2, d, dt, axis, out);
+    KCK();
+}
+
+extern "C" int mm2d_k_ghat_2d(int nx, int ny, int nv1, int nv2, const double* M, const double* rho,
+                              const double* u1, const double* u2, const double* T,
+                              const double* s11, const double* s12, const double* gT1,
+                              const double* gT2, const double* tau, const double* v1,
+                              const double* v2, double* out, void* stream) {
+    (void)rho;
+    kc_ghat<<<nblk((size_t)nx * ny * nv1 * nv2), 256, 0, (cudaStream_t)stream>>>(
+        nx * ny, nv1, nv2, M, u1, u2, T, s11, s12, gT1, gT2, tau, v1, v2, out);
+    KCK();
+}
+
+extern "C" int mm2d_k_add_gaussian_term_2d(int nx, int ny, int nv1, int nv2, double* Ghat,
+                                           const double* M, const double* rho, const double* u1,
+                                           const double* u2, const double* m11, const double* m12,
+                                           const double* m22, double eps, const double* v1,
+                                           const double* v2, void* stream) {
+    kc_gauss<<<nblk((size_t)nx * ny * nv1 * nv2), 256, 0, (cudaStream_t)stream>>>(
+        nx * ny, nv1, nv2, Ghat, M, rho, u1, u2, m11, m12, m22, eps, v1, v2);
+    KCK();
+}
+
+extern "C" int mm2d_k_add_lowrank_4d(int nx, int ny, int nv1, int nv2, double* out, int nterms,
+                                     const double* coeffs, const double* shapes, void* stream) {
+    kc_lowrank<<<nblk((size_t)nx * ny * nv1 * nv2), 256, 0, (cudaStream_t)stream>>>(
+        nx * ny, nv1 * nv2, out, nterms, coeffs, shapes);
+    KCK();
+}
+
+extern "C" int mm2d_k_relax_2d(int nx, int ny, int nv1, int nv2, const double* G,
+                               const double* Ghat, const double* tau, double dt, double eps,
+                               double* out, void* stream) {
+    kc_relax<<<nblk((size_t)nx * ny * nv1 * nv2), 256, 0, (cudaStream_t)stream>>>(
+        nx * ny, nv1 * nv2, G, Ghat, tau, dt, eps, out);
+    KCK();
+}
+
+extern "C" int mm2d_k_heat_tensor_2d(int nx, int ny, int nv1, int nv2, const double* G,
+                                     const double* u1, const double* u2, const double* v1,
+                                     const double* v2, double dv, double eps, double* H,
+                                     void* stream) {
+    kc_heat<<<nx * ny, 128, 0, (cudaStream_t)stream>>>(nx * ny, nv1, nv2, G, u1, u2, v1, v2,
+                                                       eps * dv, H);
+    KCK();
+}
+
+extern "C" int mm2d_k_upwind_z_1d(int nx, int nv, const double* G_ext, const double* v, double dx,
+                                  double* Z, void* stream) {
+    kc_upwind1d<<<nblk((size_t)nx * nv), 256, 0, (cudaStream_t)stream>>>(nx, nv, G_ext, v, dx, Z);
+    KCK();
+}
+
+extern "C" int mm2d_k_project_field_1d(int nx, int nv, const double* F, const double* M,
+                                       const double* rho, const double* u, const double* T,
+                                       const double* v, double dv, double* out, void* stream) {
+    kc_project1d<<<nx, 64, 0, (cudaStream_t)stream>>>(nv, F, M, rho, u, T, v, dv, out);
+    KCK();
+}

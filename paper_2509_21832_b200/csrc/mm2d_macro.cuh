@@ -1,0 +1,238 @@
+// Macro update: Strang-split TR-BDF2 pressure relaxation around KFVS x and y
+// sweeps of the 6-moment system, with the micro-supplied heat tensor as
+// interface-averaged sources (macro2d.py:224-240).
+//
+// Two kernels, one thread per cell:
+//   k_macro_x: Q* = relax(Q^n) on the 3-cell x stencil, KFVS x-fluxes,
+//              heat divergence -> Q** (written to the Qx ring; also on the
+//              ghost rows when the y face is a received halo, like the
+//              worker-grid's extended-range x-sweep, parallel.py:305-313)
+//   k_macro_y: KFVS y-fluxes on Q**, heat divergence, [+dt*source],
+//              final relax -> Q^{n+1}
+// The macro state is ~1% of the bytes of G, so these are latency-bound
+// tiny kernels; the arithmetic mirrors the reference's NumPy expression
+// order so results agree to a few ulps.
+#pragma once
+#include "mm2d_common.cuh"
+#include "mm2d_prep.cuh"
+
+namespace mm2d {
+
+struct MacroArgs {
+    Geometry g;
+    const double* Qr;       // ring Q^n
+    const double* Hr;       // ring heat tensor (AoS)
+    double* Qx;             // ring Q** (x-swept)
+    double* Qout;           // (bx, by, 6)
+    const double* qsrc;     // (bx, by, 6) or null
+    unsigned long long* err;
+    double dt, eps, nu, rx, ry;   // rx = dt/dx, ry = dt/dy
+    int tau_kind;
+    double tau_value;
+    unsigned step;
+};
+
+// relax_pressure_2d (macro2d.py:55-70) on one cell
+__device__ __forceinline__ void relax_cell(const MacroArgs& a, const double* q, double* o) {
+    double rho, u1, u2, t11, t12, t22;
+    prims_of(q, rho, u1, u2, t11, t12, t22);
+    const double T = 0.5 * (t11 + t22);
+    const double tau = tau_model(a.tau_kind, a.tau_value, rho, T);
+    const double z = tau * (1.0 - a.nu) * a.dt;
+    const double e2 = 48.0 * a.eps * a.eps;
+    const double W = (e2 - 10.0 * z * a.eps) / (e2 + 14.0 * z * a.eps + z * z);
+    const double p11 = rho * t11, p12 = rho * t12, p22 = rho * t22;
+    o[0] = q[0]; o[1] = q[1]; o[2] = q[2];
+    o[3] = rho * u1 * u1 + 0.5 * ((1.0 + W) * p11 + (1.0 - W) * p22);
+    o[4] = rho * u1 * u2 + W * p12;
+    o[5] = rho * u2 * u2 + 0.5 * ((1.0 - W) * p11 + (1.0 + W) * p22);
+}
+
+// pressure-primitive state (rho, u1, u2, P11, P12, P22) of a conserved
+// vector (_pressure_fields, macro2d.py:201-203)
+__device__ __forceinline__ void pstate(const double* q, double* s) {
+    double rho, u1, u2, t11, t12, t22;
+    prims_of(q, rho, u1, u2, t11, t12, t22);
+    s[0] = rho; s[1] = u1; s[2] = u2;
+    s[3] = rho * t11; s[4] = rho * t12; s[5] = rho * t22;
+}
+
+// validity of a conserved vector (primitives_2d checks)
+__device__ __forceinline__ int bad_state(const double* q) {
+    if (!(q[0] > 0.0)) return 1;
+    double rho, u1, u2, t11, t12, t22;
+    prims_of(q, rho, u1, u2, t11, t12, t22);
+    const double tol = 1e-14 * (t11 + t22);
+    const double det = t11 * t22 - t12 * t12;
+    return ((t11 <= tol) || (det <= tol * tol)) ? 2 : 0;
+}
+
+// diffuse-wall ghost pressure state from the current-stage edge state
+// (_extended_states, macro2d.py:153-181 with wall_ghost_state_2d)
+__device__ __forceinline__ void wall_pstate(const Geometry& g, int face, const double* edge,
+                                            double* s) {
+    const double rho = edge[0];
+    const double t11 = edge[3] / rho, t22 = edge[5] / rho;
+    const double Tw = g.wallT[face], U = g.wallU[face];
+    const double sign = (face == 0 || face == 2) ? -1.0 : 1.0;
+    double rw;
+    if (face < 2) { rw = wall_density(rho, edge[1], t11, Tw, sign); s[1] = 0.0; s[2] = U; }
+    else { rw = wall_density(rho, edge[2], t22, Tw, sign); s[1] = U; s[2] = 0.0; }
+    s[0] = rw; s[3] = rw * Tw; s[4] = rw * 0.0; s[5] = rw * Tw;
+}
+
+// one side's share of the KFVS flux: _split_parts_x/_y + _kfvs
+// (macro2d.py:102-138), sgn = +1 for the left/lower state, -1 for right/upper
+template <int AXIS>
+__device__ __forceinline__ void kfvs_half(const double* s, double sgn, double* out) {
+    const double rho = s[0], u1 = s[1], u2 = s[2], p11 = s[3], p12 = s[4], p22 = s[5];
+    double a, b, J[6], K[6];
+    if (AXIS == 0) {
+        a = sqrt(2.0 * p11 / (kPi * rho)) * exp(-rho * u1 * u1 / (2.0 * p11));
+        b = erf(u1 * sqrt(rho / (2.0 * p11)));
+        J[0] = rho; J[1] = rho * u1; J[2] = rho * u2;
+        J[3] = rho * u1 * u1 + 2.0 * p11;
+        J[4] = rho * u1 * u2 + 2.0 * p12;
+        J[5] = rho * u2 * u2 + p22 + p12 * p12 / p11;
+        K[0] = rho * u1; K[1] = rho * u1 * u1 + p11; K[2] = rho * u1 * u2 + p12;
+        K[3] = rho * (u1 * u1 * u1) + 3.0 * u1 * p11;
+        K[4] = rho * u1 * u1 * u2 + u2 * p11 + 2.0 * u1 * p12;
+        K[5] = rho * u1 * u2 * u2 + u1 * p22 + 2.0 * u2 * p12;
+    } else {
+        a = sqrt(2.0 * p22 / (kPi * rho)) * exp(-rho * u2 * u2 / (2.0 * p22));
+        b = erf(u2 * sqrt(rho / (2.0 * p22)));
+        J[0] = rho; J[1] = rho * u1; J[2] = rho * u2;
+        J[3] = rho * u1 * u1 + p11 + p12 * p12 / p22;
+        J[4] = rho * u1 * u2 + 2.0 * p12;
+        J[5] = rho * u2 * u2 + 2.0 * p22;
+        K[0] = rho * u2; K[1] = rho * u1 * u2 + p12; K[2] = rho * u2 * u2 + p22;
+        K[3] = rho * u1 * u1 * u2 + u2 * p11 + 2.0 * u1 * p12;
+        K[4] = rho * u1 * u2 * u2 + u1 * p22 + 2.0 * u2 * p12;
+        K[5] = rho * (u2 * u2 * u2) + 3.0 * u2 * p22;
+    }
+    const double sa = sgn * a, sb = 1.0 + sgn * b;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) out[m] = 0.5 * (sa * J[m] + sb * K[m]);
+}
+
+__global__ void k_macro_x(MacroArgs a) {
+    const Geometry& g = a.g;
+    if (*a.err != kNoError) return;
+    const int jlo = g.qylo == GM_HALO ? -1 : 0;
+    const int jhi = g.qyhi == GM_HALO ? g.by : g.by - 1;
+    const int nrow = jhi - jlo + 1;
+    const int n = g.bx * nrow;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = t / nrow, j = jlo + t % nrow;
+        const bool own = j >= 0 && j < g.by;
+        double qc[6], ql[6], qr[6];
+        relax_cell(a, a.Qr + 6 * ring_index(g, i, j), qc);
+        if (own) {
+            const int bs = bad_state(qc);
+            if (bs) {
+                const unsigned long long gcell =
+                    (unsigned long long)(g.i0 + i) * g.ny + (unsigned long long)(g.j0 + j);
+                atomicMin(a.err, err_key(a.step, bs == 1 ? ES_XS_RHO : ES_XS_SPD, gcell));
+            }
+        }
+        double sc[6], sl[6], sr[6];
+        pstate(qc, sc);
+        // left neighbour state
+        if (i == 0 && g.wall[0]) wall_pstate(g, 0, sc, sl);
+        else { relax_cell(a, a.Qr + 6 * ring_index(g, i - 1, j), ql); pstate(ql, sl); }
+        if (i == g.bx - 1 && g.wall[1]) wall_pstate(g, 1, sc, sr);
+        else { relax_cell(a, a.Qr + 6 * ring_index(g, i + 1, j), qr); pstate(qr, sr); }
+        double Ll[6], Rc[6], Lc[6], Rr[6];
+        kfvs_half<0>(sl, 1.0, Ll);
+        kfvs_half<0>(sc, -1.0, Rc);
+        kfvs_half<0>(sc, 1.0, Lc);
+        kfvs_half<0>(sr, -1.0, Rr);
+        double* o = a.Qx + 6 * ring_index(g, i, j);
+#pragma unroll
+        for (int m = 0; m < 6; ++m) {
+            const double Fm = (0.0 + Ll[m]) + Rc[m];
+            const double Fp = (0.0 + Lc[m]) + Rr[m];
+            o[m] = qc[m] - a.rx * (Fp - Fm);
+        }
+        // heat: interface means of H111, H112, H122 (x-sweep sources)
+        const double* hc = a.Hr + 4 * ring_index(g, i, j);
+        const double* hl = a.Hr + 4 * ring_index(g, i - 1, j);
+        const double* hr = a.Hr + 4 * ring_index(g, i + 1, j);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double hp = 0.5 * (hr[c] + hc[c]);
+            const double hm = 0.5 * (hc[c] + hl[c]);
+            o[3 + c] -= a.rx * (hp - hm);
+        }
+    }
+}
+
+__global__ void k_macro_y(MacroArgs a) {
+    const Geometry& g = a.g;
+    if (*a.err != kNoError) return;
+    const int n = g.bx * g.by;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = t / g.by, j = t % g.by;
+        const unsigned long long gcell =
+            (unsigned long long)(g.i0 + i) * g.ny + (unsigned long long)(g.j0 + j);
+        const double* qc = a.Qx + 6 * ring_index(g, i, j);
+        {
+            const int bs = bad_state(qc);
+            if (bs) atomicMin(a.err, err_key(a.step, bs == 1 ? ES_YS_RHO : ES_YS_SPD, gcell));
+        }
+        double sc[6], sd[6], su[6];
+        pstate(qc, sc);
+        // lower neighbour
+        if (j == 0 && g.qylo != GM_HALO && g.qylo != GM_WRAP) {
+            if (g.wall[2]) wall_pstate(g, 2, sc, sd);
+            else for (int m = 0; m < 6; ++m) sd[m] = sc[m];
+        } else {
+            const int jj = (j == 0 && g.qylo == GM_WRAP) ? g.by - 1 : j - 1;
+            pstate(a.Qx + 6 * ring_index(g, i, jj), sd);
+        }
+        if (j == g.by - 1 && g.qyhi != GM_HALO && g.qyhi != GM_WRAP) {
+            if (g.wall[3]) wall_pstate(g, 3, sc, su);
+            else for (int m = 0; m < 6; ++m) su[m] = sc[m];
+        } else {
+            const int jj = (j == g.by - 1 && g.qyhi == GM_WRAP) ? 0 : j + 1;
+            pstate(a.Qx + 6 * ring_index(g, i, jj), su);
+        }
+        double Ld[6], Rc[6], Lc[6], Ru[6];
+        kfvs_half<1>(sd, 1.0, Ld);
+        kfvs_half<1>(sc, -1.0, Rc);
+        kfvs_half<1>(sc, 1.0, Lc);
+        kfvs_half<1>(su, -1.0, Ru);
+        double q3[6];
+#pragma unroll
+        for (int m = 0; m < 6; ++m) {
+            const double Fm = (0.0 + Ld[m]) + Rc[m];
+            const double Fp = (0.0 + Lc[m]) + Ru[m];
+            q3[m] = qc[m] - a.ry * (Fp - Fm);
+        }
+        const double* hc = a.Hr + 4 * ring_index(g, i, j);
+        const double* hd = a.Hr + 4 * ring_index(g, i, j - 1);
+        const double* hu = a.Hr + 4 * ring_index(g, i, j + 1);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double hp = 0.5 * (hu[c + 1] + hc[c + 1]);
+            const double hm = 0.5 * (hc[c + 1] + hd[c + 1]);
+            q3[3 + c] -= a.ry * (hp - hm);
+        }
+        if (a.qsrc) {
+            const double* s = a.qsrc + 6 * ((size_t)i * g.by + j);
+#pragma unroll
+            for (int m = 0; m < 6; ++m) q3[m] = q3[m] + a.dt * s[m];
+        }
+        double* qo = a.Qout + 6 * ((size_t)i * g.by + j);
+        const int bs3 = bad_state(q3);
+        if (bs3) {
+            // keep Q*** so the host can report the offending value
+            atomicMin(a.err, err_key(a.step, bs3 == 1 ? ES_RL_RHO : ES_RL_SPD, gcell));
+            for (int m = 0; m < 6; ++m) qo[m] = q3[m];
+        } else {
+            relax_cell(a, q3, qo);
+        }
+    }
+}
+
+}  // namespace mm2d

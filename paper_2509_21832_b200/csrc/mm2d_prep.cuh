@@ -1,0 +1,228 @@
+// Ring fill and per-cell preparation kernels (macro state at t^n).
+#pragma once
+#include "mm2d_common.cuh"
+
+namespace mm2d {
+
+// Resolve ring cell (i, j) of a field whose ghost rules are (mxlo, mxhi,
+// mylo, myhi) -- the rules of extract_ring (parallel.py:109-150), which for
+// a single rank reduce to the serial ghost rules (boundary.py:181-241):
+// y is resolved first, then x within the resolved row.
+//   returns 0: interior cell (si, sj) of the source block
+//           1: ring cell (si, sj) that holds received halo data
+//           2: zero
+enum { RS_INTERIOR = 0, RS_RING = 1, RS_ZERO = 2 };
+
+__device__ __forceinline__ int resolve_ring(int bx, int by, int mxlo, int mxhi, int mylo,
+                                            int myhi, int i, int j, int& si, int& sj) {
+    bool yhalo = false;
+    int jj = j;
+    if (j < 0 || j >= by) {
+        const int m = j < 0 ? mylo : myhi;
+        if (m == GM_ZERO) return RS_ZERO;
+        if (m == GM_HALO) yhalo = true;
+        else if (m == GM_WRAP) jj = (j + by) % by;
+        else jj = j < 0 ? 0 : by - 1;
+    }
+    int ii = i;
+    if (i < 0 || i >= bx) {
+        const int m = i < 0 ? mxlo : mxhi;
+        if (m == GM_ZERO) return RS_ZERO;
+        if (m == GM_HALO) { si = i; sj = jj; return RS_RING; }
+        if (m == GM_WRAP) ii = (i + bx) % bx;
+        else ii = i < 0 ? 0 : bx - 1;
+    }
+    si = ii; sj = jj;
+    return yhalo ? RS_RING : RS_INTERIOR;
+}
+
+// Fill the ghost ring of Qr from the owned block Q (bx, by, 6).  Cells that
+// resolve to themselves as received halo data are left untouched.
+__global__ void k_fill_qring(Geometry g, const double* __restrict__ Q, double* __restrict__ Qr,
+                             const unsigned long long* __restrict__ err) {
+    if (*err != kNoError) return;   // keep the failing step's inputs intact
+    const int n = (g.bx + 2) * (g.by + 2);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
+        int si, sj;
+        const int rs = resolve_ring(g.bx, g.by, g.qxlo, g.qxhi, g.qylo, g.qyhi, i, j, si, sj);
+        double* dst = Qr + 6 * t;
+        if (rs == RS_INTERIOR) {
+            const double* src = Q + 6 * ((size_t)si * g.by + sj);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) dst[c] = src[c];
+        } else if (rs == RS_RING) {
+            if (si == i && sj == j) continue;   // received directly
+            const double* src = Qr + 6 * ring_index(g, si, sj);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) dst[c] = src[c];
+        } else {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) dst[c] = 0.0;
+        }
+    }
+}
+
+// Fill the ghost ring of Hr (owned part written by the micro kernel).
+// Heat ghosts: periodic wrap, extrapolate copy, wall zero, i.e. the rules of
+// interface_heat_2d (boundary.py:224-241): the interface value is the mean
+// of the two neighbours, which at a wall is half the edge value.
+__global__ void k_fill_hring(Geometry g, double* __restrict__ Hr) {
+    const int n = (g.bx + 2) * (g.by + 2);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
+        if (i >= 0 && i < g.bx && j >= 0 && j < g.by) continue;
+        int si, sj;
+        const int rs = resolve_ring(g.bx, g.by, g.hxlo, g.hxhi, g.hylo, g.hyhi, i, j, si, sj);
+        double* dst = Hr + 4 * t;
+        if (rs == RS_ZERO) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dst[c] = 0.0;
+        } else {
+            if (rs == RS_RING && si == i && sj == j) continue;
+            const double* src = Hr + 4 * ring_index(g, si, sj);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dst[c] = src[c];
+        }
+    }
+}
+
+struct PrepArgs {
+    Geometry g;
+    const double* Qr;
+    CellPar* P;
+    unsigned long long* err;      // sticky error key
+    unsigned long long* iso;      // [4]: max|m11-T|, max|m12|, max|m22-T|, max T (bit patterns)
+    double dt, eps, nu, dv;
+    int tau_kind;
+    double tau_value;
+    unsigned step;
+    int gauss;                    // nu != 0
+};
+
+__device__ __forceinline__ double tau_model(int kind, double value, double rho, double T) {
+    switch (kind) {
+        case 0: return 3.2 * sqrt(T / (2.0 * kPi));            // hard_sphere_1d
+        case 1: return rho * T;                                // pressure_1d
+        case 2: return (0.4625 * kPi) * rho;                   // esbgk_2d
+        case 3: return (3.0 * kPi * 0.436 / sqrt(2.0)) * rho;  // bgk_2d
+        default: return value;                                 // constant
+    }
+}
+
+// wall_density_ratio_2d (boundary.py:248-260) times rho
+__device__ __forceinline__ double wall_density(double rho, double ua, double taa, double Tw,
+                                               double sign) {
+    double R = sqrt(taa / Tw) * exp(-ua * ua / (2.0 * taa)) +
+               ua * sqrt(kPi / (2.0 * Tw)) * (erf(ua / sqrt(2.0 * taa)) + sign);
+    return rho * R;
+}
+
+__device__ __forceinline__ void prims_of(const double* q, double& rho, double& u1, double& u2,
+                                         double& t11, double& t12, double& t22) {
+    rho = q[0];
+    u1 = q[1] / rho;
+    u2 = q[2] / rho;
+    t11 = q[3] / rho - u1 * u1;
+    t12 = q[4] / rho - u1 * u2;
+    t22 = q[5] / rho - u2 * u2;
+}
+
+// Per ring cell: primitives, tau, Maxwellian and Gaussian prefactors, relax
+// weights; per owned cell also the centred gradients (micro2d.py:37-60),
+// the modified tensor with its SPD check (gas_state.py:138-146), the
+// isotropy maxima (micro2d.py:63-67) and the diffuse-wall ghost densities
+// of edge cells (boundary.py:248-290).
+__global__ void k_prep(PrepArgs a) {
+    const Geometry& g = a.g;
+    if (*a.err != kNoError) return;
+    const int n = (g.bx + 2) * (g.by + 2);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
+        const bool own = i >= 0 && i < g.bx && j >= 0 && j < g.by;
+        const double* q = a.Qr + 6 * t;
+        CellPar P;
+        double rho, u1, u2, t11, t12, t22;
+        rho = q[0];
+        const unsigned long long gcell =
+            (unsigned long long)(g.i0 + i) * g.ny + (unsigned long long)(g.j0 + j);
+        if (own && !(rho > 0.0)) atomicMin(a.err, err_key(a.step, ES_PRIM_RHO, gcell));
+        prims_of(q, rho, u1, u2, t11, t12, t22);
+        const double T = 0.5 * (t11 + t22);
+        if (own) {
+            const double tol = 1e-14 * (t11 + t22);
+            const double det = t11 * t22 - t12 * t12;
+            if ((t11 <= tol) || (det <= tol * tol)) atomicMin(a.err, err_key(a.step, ES_PRIM_SPD, gcell));
+        }
+        P.rho = rho; P.u1 = u1; P.u2 = u2; P.T = T;
+        P.t11 = t11; P.t12 = t12; P.t22 = t22;
+        P.isT = 1.0 / sqrt(T);
+        P.invT = 1.0 / T;
+        P.inv2T = 1.0 / (2.0 * T);
+        P.pref = rho / (2.0 * kPi * T);
+        const double tau = tau_model(a.tau_kind, a.tau_value, rho, T);
+        P.tau = tau;
+        P.invtau = 1.0 / tau;
+        P.scale = a.dv / rho;
+        const double denom = a.eps + a.dt * tau;
+        P.wg = a.eps / denom;
+        P.wh = a.dt * tau / denom;
+        P.s11 = P.s12 = P.gT1 = P.gT2 = 0.0;
+        P.m11 = P.m12 = P.m22 = 0.0;
+        P.gpref = P.gq11 = P.gq22 = P.gq12 = 0.0;
+        P.rw[0] = P.rw[1] = P.rw[2] = P.rw[3] = 0.0;
+        P.pad = 0.0;
+        if (a.gauss) {
+            const double m11 = (1.0 - a.nu) * T + a.nu * t11;
+            const double m12 = a.nu * t12;
+            const double m22 = (1.0 - a.nu) * T + a.nu * t22;
+            const double det = m11 * m22 - m12 * m12;
+            P.m11 = m11; P.m12 = m12; P.m22 = m22;
+            P.gpref = rho / (2.0 * kPi * sqrt(det));
+            P.gq11 = -0.5 * m22 / det;   // coefficient of W1^2 in the exponent
+            P.gq22 = -0.5 * m11 / det;   // coefficient of W2^2
+            P.gq12 = m12 / det;          // coefficient of W1 W2
+            if (own) {
+                const double tol = 1e-14 * (m11 + m22);
+                if ((m11 <= tol) || (det <= tol * tol))
+                    atomicMin(a.err, err_key(a.step, ES_MOD_SPD, gcell));
+                if (a.eps < 1e-10) {
+                    atomic_max_pos(&a.iso[0], fabs(m11 - T));
+                    atomic_max_pos(&a.iso[1], fabs(m12));
+                    atomic_max_pos(&a.iso[2], fabs(m22 - T));
+                    atomic_max_pos(&a.iso[3], T > 0.0 ? T : 0.0);
+                }
+            }
+        }
+        if (own) {
+            // centred differences over the ring (extend_macro_scalar_2d:
+            // wrap for periodic, copy otherwise)
+            double r_, xu1[2], xu2[2], xT[2], yu1[2], yu2[2], yT[2];
+            double a11, a12, a22;
+            for (int s = 0; s < 2; ++s) {
+                const double* qx = a.Qr + 6 * ring_index(g, i + (s ? 1 : -1), j);
+                prims_of(qx, r_, xu1[s], xu2[s], a11, a12, a22);
+                xT[s] = 0.5 * (a11 + a22);
+                const double* qy = a.Qr + 6 * ring_index(g, i, j + (s ? 1 : -1));
+                prims_of(qy, r_, yu1[s], yu2[s], a11, a12, a22);
+                yT[s] = 0.5 * (a11 + a22);
+            }
+            const double du1x = (xu1[1] - xu1[0]) / (2.0 * g.dx);
+            const double du2x = (xu2[1] - xu2[0]) / (2.0 * g.dx);
+            const double du1y = (yu1[1] - yu1[0]) / (2.0 * g.dy);
+            const double du2y = (yu2[1] - yu2[0]) / (2.0 * g.dy);
+            P.s11 = du1x - du2y;
+            P.s12 = du1y + du2x;
+            P.gT1 = (xT[1] - xT[0]) / (2.0 * g.dx);
+            P.gT2 = (yT[1] - yT[0]) / (2.0 * g.dy);
+            // wall ghost densities of edge cells (zero-mass-flux closure)
+            if (g.wall[0] && i == 0) P.rw[0] = wall_density(rho, u1, t11, g.wallT[0], -1.0);
+            if (g.wall[1] && i == g.bx - 1) P.rw[1] = wall_density(rho, u1, t11, g.wallT[1], 1.0);
+            if (g.wall[2] && j == 0) P.rw[2] = wall_density(rho, u2, t22, g.wallT[2], -1.0);
+            if (g.wall[3] && j == g.by - 1) P.rw[3] = wall_density(rho, u2, t22, g.wallT[3], 1.0);
+        }
+        reinterpret_cast<CellPar*>(a.P)[t] = P;
+    }
+}
+
+}  // namespace mm2d

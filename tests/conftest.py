@@ -1,0 +1,82 @@
+"""Shared fixtures.  ``-m gpu`` tests need a B200 (they run the CUDA path
+through the C ABI); everything else runs on the CPU (oracle vs reference
+goldens, host logic, ABI exports, gloo multi-process logic)."""
+
+import json
+import sys
+from pathlib import Path
+from types import SimpleNamespace as NS
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200) and libmm2d.so")
+
+
+def golden_index():
+    with open(GOLDEN / "index.json") as fh:
+        return json.load(fh)
+
+
+def golden_cases(prefix):
+    return sorted(k for k in golden_index() if k.startswith(prefix))
+
+
+def problem_from_golden(name):
+    """(mesh, bc, eps, model, params) built with this repo's drop-in API."""
+    from paper_2509_21832_b200 import (Axis, BoundarySpec2D, CollisionModel, EXTRAPOLATE,
+                                       PERIODIC, PhaseMesh, WallSpec)
+    p = golden_index()[name]
+
+    def face(f):
+        if isinstance(f, dict):
+            return WallSpec(temperature=f["wall"][0], velocity=f["wall"][1])
+        return {"periodic": PERIODIC, "extrapolate": EXTRAPOLATE}[f]
+
+    mesh = PhaseMesh(space=(Axis(0.0, 1.0, p["nx"]), Axis(0.0, 1.0, p["ny"])),
+                     velocity=(Axis(*p["vx"]), Axis(*p["vy"])))
+    bc = BoundarySpec2D(*(face(f) for f in p["faces"]))
+    model = CollisionModel(p["kind"], nu=p["nu"], value=p.get("tau_value", 0.7))
+    return mesh, bc, p["eps"], model, p
+
+
+def q_scales(Qref):
+    """Per-component error scales for moment comparisons (SURVEY 8c floors:
+    momentum uses max rho * sqrt(max T); E12 uses the diagonal maxima)."""
+    rho = Qref[..., 0]
+    u1 = Qref[..., 1] / rho
+    u2 = Qref[..., 2] / rho
+    T = 0.5 * (Qref[..., 3] / rho - u1 * u1 + Qref[..., 5] / rho - u2 * u2)
+    mom_floor = float(np.max(rho)) * float(np.sqrt(np.max(T)))
+    diag = max(float(np.max(np.abs(Qref[..., 3]))), float(np.max(np.abs(Qref[..., 5]))))
+    s = [float(np.max(np.abs(Qref[..., c]))) for c in range(6)]
+    s[1] = max(s[1], mom_floor)
+    s[2] = max(s[2], mom_floor)
+    s[4] = max(s[4], diag)
+    return np.array(s)
+
+
+def q_rel_err(Q, Qref):
+    """max over components of rel L-inf error with the floors above."""
+    sc = q_scales(Qref)
+    return max(float(np.max(np.abs(Q[..., c] - Qref[..., c]))) / sc[c] for c in range(6))
+
+
+def rel_err(a, b, floor=1e-300):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.max(np.abs(a - b))) / max(float(np.max(np.abs(b))), floor)
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle import oracle as O
+    O.build()
+    return O
