@@ -640,6 +640,12 @@ extern "C" int mm2d_check(mm2d_ctx* ctx, int* kind, int* i, int* j, double* valu
                           c.tau_kind, c.tau_value, ctx->last_dt, c.eps, d_v);
     CK(cudaMemcpy(&v, d_v, sizeof(double), cudaMemcpyDeviceToHost));
     cudaFree(d_v);
+    // report once: the next step starts from a clean error word (the
+    // reference raises per call)
+    {
+        const unsigned long long none = kNoError;
+        CK(cudaMemcpy(ctx->d_err, &none, sizeof(none), cudaMemcpyHostToDevice));
+    }
     if (kind) *kind = k;
     if (i) *i = gi;
     if (j) *j = gj;

@@ -164,22 +164,24 @@ struct NodeMap {
         if (FAST) {
 #pragma unroll
             for (int e = 0; e < NE; e += 2) {
-                const double2 x = *reinterpret_cast<const double2*>(p + node[e]);
-                v[e] = x.x; v[e + 1] = x.y;
+                if (ok[e]) {
+                    const double2 x = *reinterpret_cast<const double2*>(p + node[e]);
+                    v[e] = x.x; v[e + 1] = x.y;
+                } else { v[e] = 0.0; v[e + 1] = 0.0; }
             }
         } else {
 #pragma unroll
-            for (int e = 0; e < NE; ++e) v[e] = p[node[e]];
+            for (int e = 0; e < NE; ++e) v[e] = ok[e] ? p[node[e]] : 0.0;
         }
     }
     __device__ __forceinline__ void sstore(double* p, const double (&v)[NE]) const {
         if (FAST) {
 #pragma unroll
             for (int e = 0; e < NE; e += 2)
-                *reinterpret_cast<double2*>(p + node[e]) = make_double2(v[e], v[e + 1]);
+                if (ok[e]) *reinterpret_cast<double2*>(p + node[e]) = make_double2(v[e], v[e + 1]);
         } else {
 #pragma unroll
-            for (int e = 0; e < NE; ++e) p[node[e]] = v[e];
+            for (int e = 0; e < NE; ++e) if (ok[e]) p[node[e]] = v[e];
         }
     }
 };
@@ -461,7 +463,6 @@ __global__ void __launch_bounds__(256) k_micro(MicroArgs a) {
                 gh[b][e] = h;
             }
         }
-        strip = __syncthreads_or(strip);
         if (strip) {
             // ghat_override_2d (boundary.py:343-378) for wall-strip cells:
             // g^ = -(Mterm - Pi[Mterm]) / tau with Mterm the upwind transport

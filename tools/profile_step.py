@@ -1,0 +1,36 @@
+"""Run a few plain (non-graph) steps of a benchmark workload, for ncu.
+
+    python tools/profile_step.py [--config c2] [--steps 4]
+"""
+import argparse
+import ctypes as C
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2509_21832_b200.solver import Solver2D  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--steps", type=int, default=4)
+    args = ap.parse_args()
+    cfg = bench.make_workload(args.config)
+    s = Solver2D(cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"])
+    Q = torch.from_numpy(cfg["initial"](0, cfg["nx"], 0, cfg["ny"])).cuda()
+    G = torch.zeros((cfg["nx"], cfg["ny"], 32, 32), dtype=torch.float64, device="cuda")
+    for _ in range(args.steps):
+        Q, G, H = s.step(Q, G, cfg["dt"])
+    torch.cuda.synchronize()
+    s.check()
+    print("ok", float(Q[..., 0].sum()))
+
+
+if __name__ == "__main__":
+    main()
