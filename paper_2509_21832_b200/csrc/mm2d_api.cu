@@ -17,6 +17,7 @@
 #include "mm2d_contract.cuh"
 #include "mm2d_macro.cuh"
 #include "mm2d_micro.cuh"
+#include "mm2d_micro32.cuh"
 #include "mm2d_prep.cuh"
 
 using namespace mm2d;
@@ -37,6 +38,11 @@ struct mm2d_ctx {
     unsigned long long* d_err = nullptr;   // [0] key, [1..4] iso maxima
     // halo buffers for the micro field (multi-rank only)
     double* d_gh[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* d_wallg = nullptr;     // wall-strip targets (fast kernel)
+    double* d_zero = nullptr;      // V zeros
+    bool use32 = false;            // specialised 32 x 32 micro kernel
+    int grid32 = 1;                // persistent CTAs of k_micro32
+    int ly32 = 32;
     // context-owned state
     double* d_Qs[2] = {nullptr, nullptr};
     double* d_Gs[2] = {nullptr, nullptr};
@@ -198,6 +204,43 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         delete ctx;
         return r;
     }
+    ctx->use32 = c.nv1 == 32 && c.nv2 == 32 && getenv("MM2D_GENERIC") == nullptr;
+    if (ctx->use32) {
+        // the specialised kernel folds the upwind sign per node pair: both
+        // nodes of every (l, l+1) pair must share the sign of v2
+        const double h2 = (c.v2_max - c.v2_min) / c.nv2;
+        for (int l = 0; l < c.nv2; l += 2) {
+            const double a0 = c.v2_min + (l + 0.5) * h2, a1 = c.v2_min + (l + 1.5) * h2;
+            if ((a0 < 0.0) != (a1 < 0.0)) ctx->use32 = false;
+        }
+        // and the x upwind direction must flip exactly between k = 15 and 16
+        const double h1 = (c.v1_max - c.v1_min) / c.nv1;
+        for (int k = 0; k < c.nv1; ++k) {
+            const double vk = c.v1_min + (k + 0.5) * h1;
+            if ((vk < 0.0) != (k < 16)) ctx->use32 = false;
+        }
+    }
+    if (ctx->use32) {
+        if (cudaFuncSetAttribute(reinterpret_cast<const void*>(&m32::k_micro32),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)m32::smem_bytes_v3()) != cudaSuccess) {
+            int r = fail_cfg(ctx, "shared memory request too large for k_micro32");
+            delete ctx;
+            return r;
+        }
+        int occ = 0, nsm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, m32::k_micro32, m32::NT,
+                                                      m32::smem_bytes_v3());
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
+        const char* ly = getenv("MM2D_LY");
+        ctx->ly32 = ly ? std::max(1, atoi(ly)) : 32;
+        ctx->ly32 = std::min(ctx->ly32, g.by);
+        const long long items = (long long)((g.by + ctx->ly32 - 1) / ctx->ly32) * g.bx;
+        const char* pe = getenv("MM2D_PERSIST");
+        const bool persist = pe ? atoi(pe) != 0 : false;
+        const long long slots = (long long)std::max(occ, 1) * std::max(nsm, 1);
+        ctx->grid32 = (int)std::max(1LL, persist ? std::min(slots, items) : items);
+    }
     if (cudaFuncSetAttribute(ctx->micro_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)ctx->smem) != cudaSuccess) {
         int r = fail_cfg(ctx, "shared memory request too large for the micro kernel");
@@ -235,6 +278,13 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         CK(cudaMalloc(&ctx->d_gh[f], sizeof(double) * cells * Vs));
         CK(cudaMemset(ctx->d_gh[f], 0, sizeof(double) * cells * Vs));
     }
+    CK(cudaMalloc(&ctx->d_zero, sizeof(double) * Vs));
+    CK(cudaMemset(ctx->d_zero, 0, sizeof(double) * Vs));
+    if (ctx->use32 && (g.wall[0] || g.wall[1] || g.wall[2] || g.wall[3])) {
+        const size_t n = (size_t)(2 * g.by + 2 * g.bx) * Vs;
+        CK(cudaMalloc(&ctx->d_wallg, sizeof(double) * n));
+        CK(cudaMemset(ctx->d_wallg, 0, sizeof(double) * n));
+    }
     *out = ctx;
     return MM2D_OK;
 }
@@ -254,6 +304,8 @@ extern "C" int mm2d_destroy(mm2d_ctx* ctx) {
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     for (int f = 0; f < 4; ++f) cudaFree(ctx->d_gh[f]);
+    cudaFree(ctx->d_wallg);
+    cudaFree(ctx->d_zero);
     cudaFree(ctx->d_v1); cudaFree(ctx->d_v2); cudaFree(ctx->d_P); cudaFree(ctx->d_Qr);
     cudaFree(ctx->d_Hr); cudaFree(ctx->d_Qx); cudaFree(ctx->d_err);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -330,7 +382,17 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     ma.dt = dt; ma.eps = c.eps; ma.inveps = 1.0 / c.eps;
     ma.idx = 1.0 / g.dx; ma.idy = 1.0 / g.dy;
     ma.dv = pa.dv; ma.hfac = c.eps * pa.dv;
-    {
+    ma.wall_ghat = ctx->d_wallg;
+    ma.zero = ctx->d_zero;
+    if (ctx->use32 && nsrc == 0) {
+        if (ctx->d_wallg) {
+            m32::k_wall_ghat<<<2 * g.by + 2 * g.bx, 128, 0, s>>>(ma, ctx->d_wallg);
+            ++nl;
+        }
+        ma.ly = ctx->ly32;
+        dim3 grid(g.bx, (g.by + ctx->ly32 - 1) / ctx->ly32);
+        m32::k_micro32<<<grid, m32::NT, m32::smem_bytes_v3(), s>>>(ma);
+    } else {
         dim3 grid((g.bx + ctx->BX - 1) / ctx->BX, (g.by + ctx->ly - 1) / ctx->ly);
         void* args[] = {&ma};
         CK(cudaLaunchKernel(ctx->micro_fn, grid, dim3(ctx->NT), args, ctx->smem, s));

@@ -45,6 +45,8 @@ struct MicroArgs {
     const double* src_coeffs; // (nsrc, bx, by) or null
     const double* src_shapes; // (nsrc, V)
     int nsrc;
+    const double* wall_ghat;  // precomputed wall-strip targets (k_wall_ghat)
+    const double* zero;       // V zeros (zero ghosts of the specialised kernel)
     int ly;                   // rows per segment
     int gauss;                // nu != 0
     double dt, eps, inveps, idx, idy, dv, hfac;  // hfac = eps * dv

@@ -1,0 +1,643 @@
+// Fused micro kernel specialised for the 32 x 32 velocity grid of every
+// benchmark configuration (V = 1024 nodes per cell).  Same mathematics as the
+// generic k_micro (mm2d_micro.cuh), reorganised for the fp64 issue budget:
+//
+//  * 128 threads per CTA, 8 nodes per thread: thread t owns the 16-byte node
+//    pairs (k, l..l+1) with k = t/16 + 8p (p = 0..3) and l = 2 (t % 16), so a
+//    warp touches 512 contiguous bytes per pair and all upwind stencils are
+//    thread-local.
+//  * Everything that depends on (cell, k) or (cell, l) only -- the separable
+//    Maxwellian factors, the projection basis w1, w2, b4, the closed-form
+//    target's polynomial pieces, the separable ES-BGK Gaussian factors -- is
+//    built once per cell into shared-memory tables (K-table [32][8],
+//    L-table [8][32], Gaussian tables), so a node costs a handful of FMAs.
+//  * One block reduction per row: the y-projection sums of row j, the
+//    x-projection sums of row j+2 and the heat moments of row j-1 share it.
+//  * G* lives in a 3-row thread-private shared-memory ring; the x-stage of
+//    row j+2 first stores G - dt Z there and adds the projection one
+//    iteration later, once its sums are reduced.
+//  * Diffuse-wall strip targets (boundary.py:343-378) do not depend on G and
+//    are precomputed by k_wall_ghat into a small buffer.
+//
+// Row loop (iteration j, rows j0-3 .. j1; steps are predicated on validity):
+//   1. recon G*(j+1)   2. y-sums(j)   3. x-stage(j+2), prefetch G^n(j+3)
+//   4. reduction [y(j) | x(j+2) | H(j-1)], write H(j-1)
+//   5. G**(j), target, relax, store G^{n+1}(j), heat partials H(j)
+#pragma once
+#include "mm2d_common.cuh"
+#include "mm2d_micro.cuh"
+
+namespace mm2d {
+namespace m32 {
+
+constexpr int NV = 32;
+constexpr int V = NV * NV;
+constexpr int NT = 128;
+constexpr int NP = 4;                // node pairs per thread
+constexpr int TSLOTS = 5;            // table slots (rows j..j+3 + WAR margin)
+constexpr int KT = 0;                // K-table [32][8]
+constexpr int LT = KT + 8 * NV;      // L-table [8][32]
+constexpr int GK = LT + 8 * NV;      // Gaussian k-table [32][2] (GA, GD)
+constexpr int GL = GK + 2 * NV;      // Gaussian l-table [2][32] (GB, GR)
+constexpr int TAB = GL + 2 * NV;     // 640 doubles per cell
+enum { K_PE1, K_W1N, K_H1, K_W1, K_U, K_C, K_Q1, K_P1 };
+enum { L_E2, L_W2N, L_H2, L_W2, L_V, L_Q2, L_P2 };
+
+inline size_t smem_bytes() {
+    return sizeof(double) * (3 * V + TSLOTS * TAB + 4 * 16 + 16 + 2 * NV);
+}
+
+__device__ __forceinline__ double2 lds2(const double* p) {
+    return *reinterpret_cast<const double2*>(p);
+}
+__device__ __forceinline__ void sts2(double* p, double a, double b) {
+    *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+
+// one-row block all-reduce of 16 doubles with 4 warps: transposed butterfly
+// in the warp, per-warp partials through shared memory, 16 threads finish.
+__device__ __forceinline__ void reduce16(double (&v)[16], double* sred) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int idx = 0;
+#pragma unroll
+    for (int lvl = 0; lvl < 4; ++lvl) {
+        const int mask = 16 >> lvl;
+        const int half = 8 >> lvl;
+        const bool up = (lane & mask) != 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q < half) {
+                const double send = up ? v[q] : v[q + half];
+                const double keep = up ? v[q + half] : v[q];
+                v[q] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+            }
+        }
+        if (up) idx += half;
+    }
+    const double s = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+    if ((lane & 1) == 0) sred[warp * 16 + idx] = s;
+    __syncthreads();
+    if (threadIdx.x < 16)
+        sred[64 + threadIdx.x] = (sred[threadIdx.x] + sred[16 + threadIdx.x]) +
+                                 (sred[32 + threadIdx.x] + sred[48 + threadIdx.x]);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; q += 2) {
+        const double2 x = lds2(sred + 64 + q);
+        v[q] = x.x;
+        v[q + 1] = x.y;
+    }
+}
+
+// Row header stored in each table slot (doubles): per-cell scalars the node
+// loops need, so they come from shared memory instead of global loads.
+enum { H_SCALE, H_WG, H_MTW, H_MEW, H_GQ12, H_WH, H_N = 8 };
+constexpr int HD = TAB;              // header offset inside a slot
+constexpr int SLOT = TAB + H_N;      // doubles per table slot
+
+// exp(x) to ~1 ulp for x <= 709 (Cody-Waite reduction by ln 2 and a
+// degree-13 Taylor polynomial on |r| <= ln2/2, truncation < 5e-18); results
+// below ~1e-307 flush to zero (they only ever enter here as negligible
+// factors).  The coefficients live in the constant bank so every step is a
+// single DFMA: ~20 instructions against ~50 for libdevice exp.
+__constant__ double kExpC[14] = {   // 1/k!, k = 0..13
+    1.0, 1.0, 0.5, 1.6666666666666666667e-01, 4.1666666666666666667e-02,
+    8.3333333333333333333e-03, 1.3888888888888888889e-03, 1.9841269841269841270e-04,
+    2.4801587301587301587e-05, 2.7557319223985890653e-06, 2.7557319223985890653e-07,
+    2.5052108385441718775e-08, 2.0876756987868098979e-09, 1.6059043836821614599e-10};
+__constant__ double kLn2[3] = {1.4426950408889634074, 6.93147180559945286227e-01,
+                               2.31904681384629955842e-17};
+
+__device__ __forceinline__ double fexp(double x) {
+    const double SH = 6755399441055744.0;   // 1.5 * 2^52: round-to-int shifter
+    double t = fma(x, kLn2[0], SH);
+    const int n = __double2loint(t);
+    t -= SH;
+    double r = fma(t, -kLn2[1], x);
+    r = fma(t, -kLn2[2], r);
+    // Estrin evaluation: dependency depth 5 instead of 13
+    const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+    const double q0 = fma(kExpC[1], r, kExpC[0]), q1 = fma(kExpC[3], r, kExpC[2]);
+    const double q2 = fma(kExpC[5], r, kExpC[4]), q3 = fma(kExpC[7], r, kExpC[6]);
+    const double q4 = fma(kExpC[9], r, kExpC[8]), q5 = fma(kExpC[11], r, kExpC[10]);
+    const double q6 = fma(kExpC[13], r, kExpC[12]);
+    const double s0 = fma(q1, r2, q0), s1 = fma(q3, r2, q2), s2 = fma(q5, r2, q4);
+    const double t0 = fma(s1, r4, s0), t1 = fma(q6, r4, s2);
+    const double p = fma(t1, r8, t0);
+    const int hi = __double2hiint(p) + (n << 20);
+    return n < -1020 ? 0.0 : __hiloint2double(hi, __double2loint(p));
+}
+
+// Block all-reduce of the row's 12 sums (y | x | heat) through shared
+// memory: every thread stores its partials value-major (conflict-free 8-byte
+// stores), 96 threads each add 16 partials of one value (rotated start so a
+// warp's 16-byte loads hit 8 distinct bank groups), 8-lane shuffles finish,
+// and all threads read the 12 totals back.  Two barriers, ~50 instructions.
+constexpr int RED = 12 * NT + 16;    // doubles of reduction scratch
+
+__device__ __forceinline__ void reduce12(double (&v)[12], double* sred) {
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < 12; ++q) sred[q * NT + tid] = v[q];
+    __syncthreads();
+    if (tid < 96) {
+        const int vid = tid >> 3, seg = tid & 7;
+        const double* src = sred + vid * NT + 16 * seg;
+        double2 x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = lds2(src + 2 * ((q + seg) & 7));
+        double u[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) u[q] = x[q].x + x[q].y;
+        double acc = ((u[0] + u[1]) + (u[2] + u[3])) + ((u[4] + u[5]) + (u[6] + u[7]));
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (seg == 0) sred[12 * NT + vid] = acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 12; q += 2) {
+        const double2 x = lds2(sred + 12 * NT + q);
+        v[q] = x.x;
+        v[q + 1] = x.y;
+    }
+}
+
+// build the per-cell tables from the shared copy P of the cell's CellPar.
+// Work split so every warp does the same number of exps: warp 0 the K-table
+// (+ GD), warp 1 the L-table (+ GR), warps 2/3 the Gaussian GA / GB.
+__device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, const CellPar& P,
+                                             const double* v1s, const double* v2s, bool gauss) {
+    const int t = threadIdx.x;
+    const int m = t & 31;
+    if (t < 32) {
+        const double W1 = v1s[m] - P.u1;
+        const double W1s = W1 * W1;
+        const double w1 = W1 * P.isT;
+        const double q1 = W1s * P.inv2T - 2.0;
+        const double p1 = W1 * P.gT1 * P.invT;
+        double* K = T + KT + 8 * m;
+        sts2(K + K_PE1, P.pref * fexp(-W1s * P.inv2T), w1);
+        sts2(K + K_H1, 0.5 * w1 * w1 - 1.0, W1);
+        sts2(K + K_U, W1s * P.s11 * P.inv2T + q1 * p1, 2.0 * W1 * P.s12 * P.inv2T);
+        sts2(K + K_Q1, q1, p1);
+        if (gauss) T[GK + 2 * m + 1] = fexp(P.gq12 * W1 * (v2s[1] - v2s[0]));
+        if (m == 0) {
+            sts2(T + HD + H_SCALE, P.scale, P.wg);
+            sts2(T + HD + H_MTW, -P.invtau * P.wh, a.inveps * P.wh);
+            sts2(T + HD + H_GQ12, P.gq12, P.wh);
+        }
+    } else if (t < 64) {
+        const double W2 = v2s[m] - P.u2;
+        const double W2s = W2 * W2;
+        const double w2 = W2 * P.isT;
+        const double q2 = W2s * P.inv2T;
+        const double p2 = W2 * P.gT2 * P.invT;
+        double* L = T + LT + m;
+        L[L_E2 * NV] = fexp(-W2s * P.inv2T);
+        L[L_W2N * NV] = w2;
+        L[L_H2 * NV] = 0.5 * w2 * w2;
+        L[L_W2 * NV] = W2;
+        L[L_V * NV] = q2 * p2 - W2s * P.s11 * P.inv2T;
+        L[L_Q2 * NV] = q2;
+        L[L_P2 * NV] = p2;
+        if (gauss) T[GL + NV + m] = fexp(P.gq12 * (v1s[8] - v1s[0]) * W2);
+    } else if (gauss && t < 96) {
+        const double W1 = v1s[m] - P.u1;
+        T[GK + 2 * m] = P.gpref * a.inveps * P.wh * fexp(P.gq11 * (W1 * W1));
+    } else if (gauss) {
+        const double W2 = v2s[m] - P.u2;
+        T[GL + m] = fexp(P.gq22 * (W2 * W2));
+    }
+}
+
+// 16-byte asynchronous global -> shared copy (LDGSTS) and its fences
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+inline size_t smem_bytes_v3() {
+    return sizeof(double) * (3 * V + TSLOTS * SLOT + RED + 4 * 32 + 2 * NV + 2 * NP * NT);
+}
+
+// The host selects this kernel only when the velocity axes make the upwind
+// direction a compile-time property of the node pair: v1 < 0 exactly for
+// k < 16 (pairs p = 0, 1 difference towards the right neighbour), and both
+// nodes of every (l, l+1) pair share the sign of v2.
+__global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
+    extern __shared__ __align__(16) double smem[];
+    const Geometry& g = a.g;
+    if (*a.err != kNoError) return;
+    const int tid = threadIdx.x;
+    const int kb = tid >> 4, lb = (tid & 15) << 1;
+
+    double* ring = smem;                            // [3][V]
+    double* tabs = ring + 3 * V;                    // [TSLOTS][SLOT]
+    double* sred = tabs + TSLOTS * SLOT;            // [12][NT] partials + [12] totals
+    double* pring = sred + RED;                     // [4][32] staged CellPar rows
+    double* v1s = pring + 4 * 32;
+    double* v2s = v1s + NV;
+    if (tid < NV) v1s[tid] = a.v1[tid];
+    else if (tid < 2 * NV) v2s[tid - NV] = a.v2[tid - NV];
+
+    const bool gauss = a.gauss && !(a.eps < 1e-10 &&
+        __longlong_as_double(a.iso[0]) <= 1e-13 * __longlong_as_double(a.iso[3]) &&
+        __longlong_as_double(a.iso[1]) <= 1e-13 * __longlong_as_double(a.iso[3]) &&
+        __longlong_as_double(a.iso[2]) <= 1e-13 * __longlong_as_double(a.iso[3]));
+    __syncthreads();
+
+    // per-thread constants: node offsets and sign-folded upwind coefficients
+    // Y = c (G_self - G_upwind): the reference's v (G_i - G_{i-1}) / d for
+    // v >= 0 and v (G_{i+1} - G_i) / d for v < 0 (_core.pyx:152-168)
+    // node-pair offsets: off(p) = off0 + 256 p into a cell's block,
+    // koff(p) = koff0 + 64 p into the K-table (immediate offsets in SASS)
+    const int off0 = 32 * kb + lb;
+    const int koff0 = KT + 8 * kb;
+#define off_(p) (off0 + 256 * (p))
+#define koff_(p) (koff0 + 64 * (p))
+    double cx[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+        cx[p] = (p < 2 ? -a.dt : a.dt) * v1s[kb + 8 * p] * a.idx;
+    const bool negy = v2s[lb] < 0.0;
+    const double sy = negy ? -a.dt : a.dt;
+    const double cy0 = sy * v2s[lb] * a.idy, cy1 = sy * v2s[lb + 1] * a.idy;
+    const size_t V_ = V;
+
+    // Work items are (band, column) pieces of a.ly rows, numbered band-major
+    // so that CTAs running at the same time cover adjacent columns of the
+    // same band: the x-halo columns they read are each other's own columns,
+    // which keeps the halo re-reads in L2.  CTAs stride over the items
+    // (persistent when the grid is smaller than the item count).
+    {
+    const int i = blockIdx.x;
+    const int j0s = blockIdx.y * a.ly;
+    const int j1s = min(g.by, j0s + a.ly);
+    const int k_lo = row_kind(g, j0s - 1);          // ghost-row kinds at the piece ends
+    const int k_hi = row_kind(g, j1s);
+
+    // G^n column pointers for interior rows (stride V per row); ghost rows
+    // go through gn_cell.  Zero ghosts point at a zero row with stride 0.
+    const double* own_b = a.G + (size_t)i * g.by * V_;
+    const double* lft_b;
+    const double* rgt_b;
+    size_t lft_s = V_, rgt_s = V_;
+    if (i > 0) lft_b = own_b - (size_t)g.by * V_;
+    else if (g.xlo == GM_HALO) lft_b = a.hxlo;
+    else if (g.xlo == GM_WRAP) lft_b = a.G + (size_t)(g.bx - 1) * g.by * V_;
+    else if (g.xlo == GM_COPY) lft_b = own_b;
+    else { lft_b = a.zero; lft_s = 0; }
+    if (i < g.bx - 1) rgt_b = own_b + (size_t)g.by * V_;
+    else if (g.xhi == GM_HALO) rgt_b = a.hxhi;
+    else if (g.xhi == GM_WRAP) rgt_b = a.G;
+    else if (g.xhi == GM_COPY) rgt_b = own_b;
+    else { rgt_b = a.zero; rgt_s = 0; }
+
+    const bool on_x = (g.wall[0] && i == 0) || (g.wall[1] && i == g.bx - 1);
+    const double* wx = on_x ? a.wall_ghat + ((size_t)(i == 0 ? 0 : 1) * g.by) * V_ : nullptr;
+    double* out_b = a.Gout + (size_t)i * g.by * V_;
+    const double* wb = g.wall[2] ? a.wall_ghat + ((size_t)2 * g.by + i) * V_ : nullptr;
+    const double* wt = g.wall[3] ? a.wall_ghat + ((size_t)2 * g.by + g.bx + i) * V_ : nullptr;
+
+    // rows computed by the x-stage: the contiguous range [rlo, rhi] (ghost
+    // rows that are copies or zeros excluded)
+    const int rlo = k_lo == 0 ? j0s - 1 : j0s;
+    const int rhi = k_hi == 0 ? j1s : j1s - 1;
+    auto computes = [&](int r) { return (unsigned)(r - rlo) <= (unsigned)(rhi - rlo); };
+
+    // CellPar of ring row r -> pring[r & 3], 16 threads x 16 bytes; one
+    // commit group per call so wait_group 1 leaves exactly the newest in flight
+    auto stage_par = [&](int r, bool on) {
+        if (on && tid < 16)
+            cp_async16(pring + 32 * (r & 3) + 2 * tid,
+                       reinterpret_cast<const double*>(a.P + ring_index(g, i, r)) + 2 * tid);
+        cp_async_commit();
+    };
+    __syncthreads();   // previous piece fully drained
+    stage_par(j0s - 1, computes(j0s - 1));
+    stage_par(j0s, computes(j0s));
+    cp_async_wait_all();
+    __syncthreads();
+
+    double2 pf[NP];               // prefetched own G^n of the next x-stage row
+    double* hst = pring + 4 * 32 + 2 * NV;   // [NP][NT] double2 halo staging (thread-private)
+    auto prefetch = [&](int r) {
+        const double *own, *hl, *hr;
+        if (r >= 0 && r < g.by) {
+            own = own_b + (size_t)r * V_;
+            hl = lft_b + (size_t)r * lft_s;
+            hr = rgt_b + (size_t)r * rgt_s;
+        } else {
+            own = gn_cell(a, i, r);
+            hl = gn_cell(a, i - 1, r);
+            hr = gn_cell(a, i + 1, r);
+            if (!own) own = a.zero;
+            if (!hl) hl = a.zero;
+            if (!hr) hr = a.zero;
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            pf[p] = __ldg(reinterpret_cast<const double2*>(own + off_(p)));
+            cp_async16(hst + 2 * (p * NT + tid), (p < 2 ? hr : hl) + off_(p));
+        }
+        cp_async_commit();
+    };
+
+    // rotating slot pointers: ring rows (j-1, j, j+1); table rows
+    // (j, j+1, j+2, j+3, j-1)
+    double* R0 = ring;
+    double* R1 = ring + V;
+    double* R2 = ring + 2 * V;
+    double* T0 = tabs;
+    double* T1 = tabs + SLOT;
+    double* T2 = tabs + 2 * SLOT;
+    double* T3 = tabs + 3 * SLOT;
+    double* T4 = tabs + 4 * SLOT;
+
+    double ax[4] = {0, 0, 0, 0};   // x-projection sums of the pending row
+    double hs[4] = {0, 0, 0, 0};   // heat partial sums of the previous row
+    double ty[2 * NP];              // G* - dt Z_y of the current row
+#pragma unroll
+    for (int q = 0; q < 2 * NP; ++q) ty[q] = 0.0;
+
+    for (int j = j0s - 4; j <= j1s; ++j) {
+        const int rx = j + 2;       // x-stage row
+        const int rc = j + 1;       // recon row
+        const bool row_j = j >= j0s && j < j1s;
+        // 0. tables for row j+3 (first used after this iteration's barriers);
+        //    stage the CellPar of row j+4 for the next iteration's builder
+        if (computes(j + 3))
+            build_tables(a, T3, *reinterpret_cast<const CellPar*>(pring + 32 * ((j + 3) & 3)),
+                         v1s, v2s, gauss);
+        stage_par(j + 5, computes(j + 5));
+        // 1. recon G*(j+1) = (G - dt Z) + dt Zhat_x
+        if (computes(rc)) {
+            const double* T = T1;
+            const double sc = T[HD + H_SCALE];
+            const double a1 = ax[0] * sc, a2 = ax[1] * sc, a3 = ax[2] * sc, a4 = ax[3] * sc;
+            const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
+            const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
+            const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
+            const double b0 = fma(w2.x, a3, h2.x * a4), b1 = fma(w2.y, a3, h2.y * a4);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const double2 kw = lds2(T + koff_(p) + K_PE1);   // pE1, w1
+                const double h1 = T[koff_(p) + K_H1];
+                const double al = fma(kw.y, a2, fma(h1, a4, a1));
+                const double2 t = lds2(R2 + off_(p));
+                sts2(R2 + off_(p), fma((al + b0) * kw.x, E2.x, t.x),
+                     fma((al + b1) * kw.x, E2.y, t.y));
+            }
+        } else if ((rc == j1s && k_hi != 0) || (rc == j0s - 1 && k_lo == 2)) {
+            // ghost rows: zero (wall) or copy of the adjacent owned row
+            const bool cp = rc == j1s && k_hi == 1;
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const double2 s = cp ? lds2(R1 + off_(p)) : make_double2(0.0, 0.0);
+                sts2(R2 + off_(p), s.x, s.y);
+            }
+        }
+        if (rc == j0s && k_lo == 1) {   // bottom ghost by copy, once G*(j0s) is complete
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const double2 s = lds2(R2 + off_(p));
+                sts2(R1 + off_(p), s.x, s.y);
+            }
+        }
+        double s[12];
+#pragma unroll
+        for (int q = 0; q < 12; ++q) s[q] = 0.0;
+        // 2. y-sums of row j: Y = cy (G*_j - G*_upwind)
+        if (row_j) {
+            const double* T = T0;
+            const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
+            const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
+            const double* gn = negy ? R2 : R0;
+            double c0[NP], c1[NP], c2[NP], c3[NP];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const double2 kw = lds2(T + koff_(p) + K_PE1);
+                const double h1 = T[koff_(p) + K_H1];
+                const double2 c = lds2(R1 + off_(p));
+                const double2 n = lds2(gn + off_(p));
+                const double y0 = cy0 * (c.x - n.x);
+                const double y1 = cy1 * (c.y - n.y);
+                ty[2 * p] = c.x - y0;
+                ty[2 * p + 1] = c.y - y1;
+                const double ys = y0 + y1;
+                c0[p] = ys;
+                c1[p] = kw.y * ys;
+                c2[p] = fma(w2.x, y0, w2.y * y1);
+                c3[p] = fma(h1, ys, fma(h2.x, y0, h2.y * y1));
+            }
+            s[0] = (c0[0] + c0[1]) + (c0[2] + c0[3]);
+            s[1] = (c1[0] + c1[1]) + (c1[2] + c1[3]);
+            s[2] = (c2[0] + c2[1]) + (c2[2] + c2[3]);
+            s[3] = (c3[0] + c3[1]) + (c3[2] + c3[3]);
+        }
+        // 3. x-stage of row j+2 into the slot of row j-1: G - dt Z_x
+        const bool do_x = computes(rx);
+        if (do_x) {
+            const double* T = T2;
+            const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
+            const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
+            cp_async_wait_prev();   // this row's halos (staged one iteration ago)
+            double c0[NP], c1[NP], c2[NP], c3[NP];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const double2 kw = lds2(T + koff_(p) + K_PE1);
+                const double h1 = T[koff_(p) + K_H1];
+                const double2 c = pf[p], h = lds2(hst + 2 * (p * NT + tid));
+                const double y0 = cx[p] * (c.x - h.x), y1 = cx[p] * (c.y - h.y);
+                sts2(R0 + off_(p), c.x - y0, c.y - y1);
+                const double ys = y0 + y1;
+                c0[p] = ys;
+                c1[p] = kw.y * ys;
+                c2[p] = fma(w2.x, y0, w2.y * y1);
+                c3[p] = fma(h1, ys, fma(h2.x, y0, h2.y * y1));
+            }
+            s[4] = (c0[0] + c0[1]) + (c0[2] + c0[3]);
+            s[5] = (c1[0] + c1[1]) + (c1[2] + c1[3]);
+            s[6] = (c2[0] + c2[1]) + (c2[2] + c2[3]);
+            s[7] = (c3[0] + c3[1]) + (c3[2] + c3[3]);
+        }
+        if (computes(rx + 1)) prefetch(rx + 1);
+        s[8] = hs[0]; s[9] = hs[1]; s[10] = hs[2]; s[11] = hs[3];
+        // 4. the row's block reduction; the CellPar staged one iteration
+        //    ago (row j+4) lands before it
+        cp_async_wait_prev();
+        reduce12(s, sred);
+        if (j - 1 >= j0s && j - 1 < j1s && tid < 4)
+            a.Hr[4 * ring_index(g, i, j - 1) + tid] = a.hfac * sred[12 * NT + 8 + tid];
+        if (do_x) {
+            ax[0] = s[4]; ax[1] = s[5]; ax[2] = s[6]; ax[3] = s[7];
+        }
+        // 5. G**(j), target, relax, store, heat partials
+        hs[0] = hs[1] = hs[2] = hs[3] = 0.0;
+        if (row_j) {
+            const double* T = T0;
+            const double sc = T[HD + H_SCALE];
+            const double a1 = s[0] * sc, a2 = s[1] * sc, a3 = s[2] * sc, a4 = s[3] * sc;
+            const double wg = T[HD + H_WG];
+            const double mtw = T[HD + H_MTW];
+            const double mew = T[HD + H_MEW];
+            const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
+            const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
+            const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
+            const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
+            const double2 Vl = lds2(T + LT + L_V * NV + lb);
+            const double2 q2 = lds2(T + LT + L_Q2 * NV + lb);
+            const double2 p2 = lds2(T + LT + L_P2 * NV + lb);
+            const double b0 = fma(w2.x, a3, h2.x * a4), b1 = fma(w2.y, a3, h2.y * a4);
+            const double W2xx = W2.x * W2.x, W2yy = W2.y * W2.y;
+            // wall-strip target (boundary.py:343-378), precomputed
+            const double* wsrc = wx ? wx + (size_t)j * V_ : (j == 0 ? wb : (j == g.by - 1 ? wt : nullptr));
+            // ES-BGK Gaussian: X(k, l) = exp(c12 W1 W2 / det), by recurrence
+            double2 GB = make_double2(0.0, 0.0);
+            double GR = 1.0, Xp = 0.0;
+            if (gauss) {
+                GB = lds2(T + GL + lb);
+                GR = T[GL + NV + lb];
+                Xp = fexp(T[HD + H_GQ12] * T[KT + 8 * kb + K_W1] * W2.x);
+            }
+            double* out = out_b + (size_t)j * V_;
+            double e0[NP], e1[NP], e2[NP], e3[NP];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                const double* K = T + koff_(p);
+                const double2 kw = lds2(K + K_PE1);     // pE1, w1
+                const double2 hW = lds2(K + K_H1);      // h1, W1
+                const double al = fma(kw.y, a2, fma(hW.x, a4, a1));
+                const double M0 = kw.x * E2.x, M1 = kw.x * E2.y;
+                const double gs0 = fma(al + b0, M0, ty[2 * p]);
+                const double gs1 = fma(al + b1, M1, ty[2 * p + 1]);
+                double acc0, acc1;
+                if (wsrc == nullptr) {
+                    // closed-form target (_core.pyx:220-224), factored
+                    const double2 Uc = lds2(K + K_U);   // U, c
+                    const double2 qp = lds2(K + K_Q1);  // q1, p1
+                    double P0 = Uc.x + Vl.x, P1 = Uc.x + Vl.y;
+                    P0 = fma(Uc.y, W2.x, P0); P1 = fma(Uc.y, W2.y, P1);
+                    P0 = fma(qp.x, p2.x, P0); P1 = fma(qp.x, p2.y, P1);
+                    P0 = fma(qp.y, q2.x, P0); P1 = fma(qp.y, q2.y, P1);
+                    acc0 = P0 * (M0 * mtw);
+                    acc1 = P1 * (M1 * mtw);
+                    if (gauss) {
+                        // (Gaussian - M)/eps (x wh), Gaussian = GA GB X
+                        const double2 gad = lds2(T + GK + 2 * (kb + 8 * p));   // GA', GD
+                        acc0 = fma(gad.x * GB.x, Xp, fma(M0, -mew, acc0));
+                        acc1 = fma(gad.x * GB.y, Xp * gad.y, fma(M1, -mew, acc1));
+                    }
+                } else {
+                    const double2 w = __ldg(reinterpret_cast<const double2*>(wsrc + off_(p)));
+                    const double wh = T[HD + H_WH];
+                    acc0 = wh * w.x;
+                    acc1 = wh * w.y;
+                }
+                const double o0 = fma(wg, gs0, acc0), o1 = fma(wg, gs1, acc1);
+                *reinterpret_cast<double2*>(out + off_(p)) = make_double2(o0, o1);
+                // heat moments about u^n (_core.pyx:303-321)
+                const double W1 = hW.y, W11 = W1 * W1;
+                const double t10 = W11 * o0, t11 = W11 * o1;
+                const double t20 = W2xx * o0, t21 = W2yy * o1;
+                e0[p] = (t10 + t11) * W1;
+                e1[p] = fma(t10, W2.x, t11 * W2.y);
+                e2[p] = (t20 + t21) * W1;
+                e3[p] = fma(t20, W2.x, t21 * W2.y);
+                Xp *= GR;
+            }
+            hs[0] = (e0[0] + e0[1]) + (e0[2] + e0[3]);
+            hs[1] = (e1[0] + e1[1]) + (e1[2] + e1[3]);
+            hs[2] = (e2[0] + e2[1]) + (e2[2] + e2[3]);
+            hs[3] = (e3[0] + e3[1]) + (e3[2] + e3[3]);
+        }
+        // rotate slots for the next row
+        {
+            double* r0 = R0; R0 = R1; R1 = R2; R2 = r0;
+            double* t0 = T0; T0 = T1; T1 = T2; T2 = T3; T3 = T4; T4 = t0;
+        }
+    }
+    }   // pieces
+}
+
+// Diffuse-wall strip targets: g^ = -(Mterm - Pi[Mterm]) / tau for every
+// wall-adjacent cell (boundary.py:343-378; _wall_maxwellian_layer 293-301,
+// extend_maxwellian_2d 304-340).  One CTA per strip cell; faces laid out
+// left (by), right (by), bottom (bx), top (bx).
+__global__ void __launch_bounds__(128) k_wall_ghat(MicroArgs a, double* out) {
+    __shared__ double sh[32];
+    const Geometry& g = a.g;
+    if (*a.err != kNoError) return;
+    const int e = blockIdx.x;
+    int f, i, j;
+    if (e < g.by) { f = 0; i = 0; j = e; }
+    else if (e < 2 * g.by) { f = 1; i = g.bx - 1; j = e - g.by; }
+    else if (e < 2 * g.by + g.bx) { f = 2; i = e - 2 * g.by; j = 0; }
+    else { f = 3; i = e - 2 * g.by - g.bx; j = g.by - 1; }
+    if (!g.wall[f]) return;
+    const CellPar& P = a.P[ring_index(g, i, j)];
+    const int nv2 = g.nv2, V = g.V;
+    double s[4] = {0, 0, 0, 0};
+    double mt[16];
+    int cnt = 0;
+    for (int n = threadIdx.x; n < V; n += blockDim.x, ++cnt) {
+        const int k = n / nv2, l = n % nv2;
+        const double v1 = a.v1[k], v2 = a.v2[l];
+        const double x1 = v1 - P.u1, x2 = v2 - P.u2;
+        const double M = P.pref * exp(-(x1 * x1 + x2 * x2) * P.inv2T);
+        double Mn[4];
+        for (int q = 0; q < 4; ++q) {
+            const int ii = i + (q == 0 ? -1 : q == 1 ? 1 : 0);
+            const int jj = j + (q == 2 ? -1 : q == 3 ? 1 : 0);
+            const bool outside = ii < 0 || ii >= g.bx || jj < 0 || jj >= g.by;
+            if (outside && g.wall[q]) {
+                const double Tw = g.wallT[q], U = g.wallU[q];
+                const double g1 = q < 2 ? 0.0 : U, g2 = q < 2 ? U : 0.0;
+                const double y1 = v1 - g1, y2 = v2 - g2;
+                Mn[q] = P.rw[q] / (2.0 * kPi * Tw) * exp(-(y1 * y1 + y2 * y2) / (2.0 * Tw));
+            } else {
+                const CellPar& Q = a.P[ring_index(g, ii, jj)];
+                const double y1 = v1 - Q.u1, y2 = v2 - Q.u2;
+                Mn[q] = Q.pref * exp(-(y1 * y1 + y2 * y2) * Q.inv2T);
+            }
+        }
+        const double vm1 = v1 < 0.0 ? v1 : 0.0, vp1 = v1 > 0.0 ? v1 : 0.0;
+        const double vm2 = v2 < 0.0 ? v2 : 0.0, vp2 = v2 > 0.0 ? v2 : 0.0;
+        const double Mt = (vm1 * (Mn[1] - M) + vp1 * (M - Mn[0])) * a.idx +
+                          (vm2 * (Mn[3] - M) + vp2 * (M - Mn[2])) * a.idy;
+        const double w1 = x1 * P.isT, w2 = x2 * P.isT;
+        const double b4 = 0.5 * (w1 * w1 + w2 * w2) - 1.0;
+        s[0] += Mt; s[1] += Mt * w1; s[2] += Mt * w2; s[3] += Mt * b4;
+        mt[cnt] = Mt;
+    }
+    double c[4];
+    for (int q = 0; q < 4; ++q) {
+        double v = warp_sum(s[q]);
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        __syncthreads();
+        if (lane == 0) sh[w] = v;
+        __syncthreads();
+        double t = 0.0;
+        for (int u = 0; u < (int)(blockDim.x >> 5); ++u) t += sh[u];
+        c[q] = t * P.scale;
+    }
+    double* o = out + (size_t)e * V;
+    cnt = 0;
+    for (int n = threadIdx.x; n < V; n += blockDim.x, ++cnt) {
+        const int k = n / nv2, l = n % nv2;
+        const double x1 = a.v1[k] - P.u1, x2 = a.v2[l] - P.u2;
+        const double M = P.pref * exp(-(x1 * x1 + x2 * x2) * P.inv2T);
+        const double w1 = x1 * P.isT, w2 = x2 * P.isT;
+        const double b4 = 0.5 * (w1 * w1 + w2 * w2) - 1.0;
+        const double pi = (c[0] + w1 * c[1] + w2 * c[2] + b4 * c[3]) * M;
+        o[n] = -(mt[cnt] - pi) * P.invtau;
+    }
+}
+
+}  // namespace m32
+}  // namespace mm2d
