@@ -107,6 +107,16 @@ int mm2d_step(mm2d_ctx *ctx, const double *d_Q, const double *d_G, double dt,
               int nsrc, const double *d_src_coeffs, const double *d_src_shapes,
               const double *d_qsrc, void *stream);
 
+/* the same step split at the heat-tensor exchange point of the block
+ * decomposition (parallel.py:384-394): phase 0 = macro ring + per-cell prep
+ * + fused micro kernel (writes G^{n+1} and the owned heat tensor), phase 1 =
+ * heat ring + KFVS/TR-BDF2 macro update.  Between them a multi-rank run
+ * exchanges the heat-tensor halo (mm2d_halo_*, field 2). */
+int mm2d_step_phase(mm2d_ctx *ctx, int phase, const double *d_Q, const double *d_G, double dt,
+                    double *d_Qout, double *d_Gout, double *d_H,
+                    int nsrc, const double *d_src_coeffs, const double *d_src_shapes,
+                    const double *d_qsrc, void *stream);
+
 /* context-owned state (ping-pong buffers in HBM) */
 int mm2d_alloc_state(mm2d_ctx *ctx);
 int mm2d_upload(mm2d_ctx *ctx, const double *h_Q, const double *h_G);
@@ -138,11 +148,17 @@ int mm2d_heat_tensor(mm2d_ctx *ctx, const double *d_G, const double *d_Q,
 int mm2d_check(mm2d_ctx *ctx, int *kind, int *i, int *j, double *value);
 int mm2d_sync(mm2d_ctx *ctx);
 
-/* multi-GPU halo exchange hooks (parallel.py:109-150 semantics).  The
- * exchange itself is driven by the host (NCCL through torch.distributed);
- * these expose the context's halo staging buffers.  Slot order: left,
- * right, bottom, top, then corners bottom-left, top-left, bottom-right,
- * top-right. */
+/* multi-GPU halo exchange hooks (extract_ring semantics, parallel.py:109-150).
+ * The transfer itself is driven by the host (NCCL send/recv through
+ * torch.distributed, or device copies between contexts of one process);
+ * these expose the context's staging buffers.  `which`: 0 = micro field G
+ * (V doubles per cell, received in place into the kernel's halo buffers),
+ * 1 = macro state Q (6), 2 = heat tensor H (4).  Slots: 0 left, 1 right,
+ * 2 bottom, 3 top, 4 bottom-left, 5 bottom-right, 6 top-left, 7 top-right;
+ * send slot s goes to the neighbour in direction s and lands in its receive
+ * slot opposite(s).  count = doubles in the slot (0 when the face is a
+ * physical boundary).  pack: G and Q from d_src (block layout), H from the
+ * heat ring; unpack scatters received Q / H ghosts into their rings. */
 int mm2d_halo_info(mm2d_ctx *ctx, int which, int slot, double **d_send,
                    double **d_recv, long long *count);
 int mm2d_halo_pack(mm2d_ctx *ctx, int which, const double *d_src, void *stream);

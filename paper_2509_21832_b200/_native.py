@@ -62,6 +62,8 @@ SIGNATURES = {
                              C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "mm2d_step": (C.c_int, [_vp, _vp, _vp, C.c_double, _vp, _vp, _vp, C.c_int,
                             _vp, _vp, _vp, _vp]),
+    "mm2d_step_phase": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_double, _vp, _vp, _vp, C.c_int,
+                                  _vp, _vp, _vp, _vp]),
     "mm2d_alloc_state": (C.c_int, [_vp]),
     "mm2d_upload": (C.c_int, [_vp, _vp, _vp]),
     "mm2d_upload_device": (C.c_int, [_vp, _vp, _vp]),

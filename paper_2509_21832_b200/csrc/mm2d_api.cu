@@ -64,6 +64,11 @@ struct mm2d_ctx {
     cudaStream_t user_stream = nullptr;
     bool have_user_stream = false;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    // halo staging (multi-rank): [field G/Q/H][slot]
+    bool halo_ready = false;
+    int halo_cells[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double* hsend[3][8] = {};
+    double* hrecv[3][8] = {};
     std::string err;
 };
 
@@ -303,6 +308,11 @@ extern "C" int mm2d_destroy(mm2d_ctx* ctx) {
     if (ctx->state_owned) cudaFree(ctx->d_Hsoa);
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+    for (int f = 0; f < 3; ++f)
+        for (int q = 0; q < 8; ++q) {
+            cudaFree(ctx->hsend[f][q]);
+            if (f > 0) cudaFree(ctx->hrecv[f][q]);
+        }
     for (int f = 0; f < 4; ++f) cudaFree(ctx->d_gh[f]);
     cudaFree(ctx->d_wallg);
     cudaFree(ctx->d_zero);
@@ -340,7 +350,8 @@ static int grid_for(long long n, int threads) {
 // enqueue one full step on `s` (graph-capturable: no host syncs)
 static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double dt, double* Qout,
                         double* Gout, double* H, int nsrc, const double* sc, const double* ss,
-                        const double* qsrc, cudaStream_t s, cudaEvent_t* ev = nullptr) {
+                        const double* qsrc, cudaStream_t s, cudaEvent_t* ev = nullptr,
+                        int phases = 3) {
 #define MARK(q) \
     if (ev) CK(cudaEventRecord(ev[q], s))
     const Geometry& g = ctx->g;
@@ -354,6 +365,7 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     }
     ctx->last_dt = dt;
     ctx->last_Qout = Qout;
+    if (phases & 1) {
     MARK(0);
     k_fill_qring<<<grid_for(ring, 256), 256, 0, s>>>(g, Q, ctx->d_Qr, ctx->d_err);
     MARK(1);
@@ -398,6 +410,9 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
         CK(cudaLaunchKernel(ctx->micro_fn, grid, dim3(ctx->NT), args, ctx->smem, s));
     }
     MARK(3);
+    nl += 3;
+    }   // phase 0: ring, prep, micro
+    if (phases & 2) {
     k_fill_hring<<<grid_for(ring, 256), 256, 0, s>>>(g, ctx->d_Hr);
     MARK(4);
     MacroArgs mc;
@@ -409,17 +424,28 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     MARK(5);
     k_macro_y<<<grid_for((long long)g.bx * g.by, 128), 128, 0, s>>>(mc);
     MARK(6);
-    nl += 6;
+    nl += 3;
     if (H) {
         k_h_soa<<<grid_for((long long)g.bx * g.by, 256), 256, 0, s>>>(g, ctx->d_Hr, H);
         ++nl;
     }
     MARK(7);
+    }   // phase 1: heat ring, macro
 #undef MARK
     CK(cudaGetLastError());
-    ctx->launches_per_step = nl;
+    if (phases == 3) ctx->launches_per_step = nl;
     if (ctx->counting) g_launches += nl;
     return MM2D_OK;
+}
+
+extern "C" int mm2d_step_phase(mm2d_ctx* ctx, int phase, const double* d_Q, const double* d_G,
+                               double dt, double* d_Qout, double* d_Gout, double* d_H, int nsrc,
+                               const double* d_src_coeffs, const double* d_src_shapes,
+                               const double* d_qsrc, void* stream) {
+    if (!ctx || (phase != 0 && phase != 1)) return fail_cfg(ctx, "phase must be 0 or 1");
+    CK(cudaSetDevice(ctx->dev));
+    return enqueue_step(ctx, d_Q, d_G, dt, d_Qout, d_Gout, d_H, nsrc, d_src_coeffs,
+                        d_src_shapes, d_qsrc, (cudaStream_t)stream, nullptr, 1 << phase);
 }
 
 extern "C" int mm2d_step(mm2d_ctx* ctx, const double* d_Q, const double* d_G, double dt,
@@ -718,18 +744,168 @@ extern "C" int mm2d_check(mm2d_ctx* ctx, int* kind, int* i, int* j, double* valu
     return MM2D_ERR_STATE;
 }
 
+// ---------------------------------------------------------------------------
+// halo exchange staging (block decomposition, parallel.py:109-150)
+// slots: 0 L, 1 R, 2 B, 3 T, 4 BL, 5 BR, 6 TL, 7 TR.  Send slot s carries
+// this block's edge cells towards neighbour s, which receives them as its
+// ghost cells of slot opposite(s).
+// ---------------------------------------------------------------------------
+static const int kOpp[8] = {1, 0, 3, 2, 7, 6, 5, 4};
+
+static bool slot_active(const Geometry& g, int s) {
+    const bool L = g.xlo == GM_HALO, R = g.xhi == GM_HALO, B = g.ylo == GM_HALO, T = g.yhi == GM_HALO;
+    switch (s) {
+        case 0: return L; case 1: return R; case 2: return B; case 3: return T;
+        case 4: return L && B; case 5: return R && B; case 6: return L && T; default: return R && T;
+    }
+}
+static int slot_cells(const Geometry& g, int s) { return s < 2 ? g.by : s < 4 ? g.bx : 1; }
+static int field_width(const Geometry& g, int f) { return f == 0 ? g.V : f == 1 ? 6 : 4; }
+
+// edge cell (send) and ghost cell (receive) of slot s, element e
+__host__ __device__ inline void slot_cell(const Geometry& g, int s, int e, bool ghost, int& i, int& j) {
+    switch (s) {
+        case 0: i = ghost ? -1 : 0; j = e; break;
+        case 1: i = ghost ? g.bx : g.bx - 1; j = e; break;
+        case 2: i = e; j = ghost ? -1 : 0; break;
+        case 3: i = e; j = ghost ? g.by : g.by - 1; break;
+        case 4: i = ghost ? -1 : 0; j = ghost ? -1 : 0; break;
+        case 5: i = ghost ? g.bx : g.bx - 1; j = ghost ? -1 : 0; break;
+        case 6: i = ghost ? -1 : 0; j = ghost ? g.by : g.by - 1; break;
+        default: i = ghost ? g.bx : g.bx - 1; j = ghost ? g.by : g.by - 1; break;
+    }
+}
+
+struct HaloDesc {
+    double* buf[8];      // staging (send) or receive buffers per slot
+    int cells[8];        // 0 when inactive
+    int width;           // doubles per cell
+};
+
+// pack edge cells of a block-layout field (G: V doubles per cell, Q: 6) or
+// of the heat ring (H: from Hr) into the send buffers
+__global__ void k_halo_pack(Geometry g, int field, const double* __restrict__ src,
+                            const double* __restrict__ Hr, HaloDesc d) {
+    const int w = d.width;
+    for (int s = 0; s < 8; ++s) {
+        if (!d.cells[s]) continue;
+        const long long n = (long long)d.cells[s] * w;
+        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+             t += (long long)gridDim.x * blockDim.x) {
+            const int e = (int)(t / w), c = (int)(t % w);
+            int i, j;
+            slot_cell(g, s, e, false, i, j);
+            d.buf[s][t] = field == 2 ? Hr[4 * ring_index(g, i, j) + c]
+                                     : src[((size_t)i * g.by + j) * w + c];
+        }
+    }
+}
+
+// scatter received Q / H ghosts into their ring
+__global__ void k_halo_unpack(Geometry g, double* __restrict__ ringbuf, HaloDesc d) {
+    const int w = d.width;
+    for (int s = 0; s < 8; ++s) {
+        if (!d.cells[s]) continue;
+        const long long n = (long long)d.cells[s] * w;
+        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+             t += (long long)gridDim.x * blockDim.x) {
+            const int e = (int)(t / w), c = (int)(t % w);
+            int i, j;
+            slot_cell(g, s, e, true, i, j);
+            ringbuf[w * ring_index(g, i, j) + c] = d.buf[s][t];
+        }
+    }
+}
+
+static int ensure_halo(mm2d_ctx* ctx) {
+    if (ctx->halo_ready) return MM2D_OK;
+    const Geometry& g = ctx->g;
+    const size_t V = (size_t)g.V;
+    for (int f = 0; f < 3; ++f)
+        for (int s = 0; s < 8; ++s) {
+            const int n = slot_active(g, s) ? slot_cells(g, s) : 0;
+            ctx->halo_cells[s] = n;
+            const size_t cnt = (size_t)n * field_width(g, f);
+            ctx->hsend[f][s] = nullptr;
+            ctx->hrecv[f][s] = nullptr;
+            if (!n) continue;
+            CK(cudaMalloc(&ctx->hsend[f][s], sizeof(double) * cnt));
+            if (f == 0) {
+                // G arrives directly in the micro kernel's halo buffers
+                double* base = nullptr;
+                switch (s) {
+                    case 0: base = ctx->d_gh[0]; break;
+                    case 1: base = ctx->d_gh[1]; break;
+                    case 2: base = ctx->d_gh[2] + V; break;
+                    case 3: base = ctx->d_gh[3] + V; break;
+                    case 4: base = ctx->d_gh[2]; break;
+                    case 5: base = ctx->d_gh[2] + (size_t)(g.bx + 1) * V; break;
+                    case 6: base = ctx->d_gh[3]; break;
+                    default: base = ctx->d_gh[3] + (size_t)(g.bx + 1) * V; break;
+                }
+                ctx->hrecv[f][s] = base;
+            } else {
+                CK(cudaMalloc(&ctx->hrecv[f][s], sizeof(double) * cnt));
+            }
+        }
+    ctx->halo_ready = true;
+    return MM2D_OK;
+}
+
 extern "C" int mm2d_halo_info(mm2d_ctx* ctx, int which, int slot, double** d_send,
                               double** d_recv, long long* count) {
-    (void)which; (void)slot; (void)d_send; (void)d_recv; (void)count;
-    return fail_cfg(ctx, "halo exchange buffers are not enabled in this build");
+    if (!ctx || which < 0 || which > 2 || slot < 0 || slot > 7) return fail_cfg(ctx, "bad halo slot");
+    CK(cudaSetDevice(ctx->dev));
+    int r = ensure_halo(ctx);
+    if (r) return r;
+    const int n = ctx->halo_cells[slot];
+    if (d_send) *d_send = ctx->hsend[which][slot];
+    if (d_recv) *d_recv = ctx->hrecv[which][slot];
+    if (count) *count = (long long)n * field_width(ctx->g, which);
+    return MM2D_OK;
 }
+
+static HaloDesc halo_desc(mm2d_ctx* ctx, int which, bool send) {
+    HaloDesc d;
+    for (int s = 0; s < 8; ++s) {
+        d.buf[s] = send ? ctx->hsend[which][s] : ctx->hrecv[which][s];
+        d.cells[s] = ctx->halo_cells[s];
+    }
+    d.width = field_width(ctx->g, which);
+    return d;
+}
+
 extern "C" int mm2d_halo_pack(mm2d_ctx* ctx, int which, const double* d_src, void* stream) {
-    (void)which; (void)d_src; (void)stream;
-    return fail_cfg(ctx, "halo exchange buffers are not enabled in this build");
+    if (!ctx || which < 0 || which > 2) return fail_cfg(ctx, "bad halo field");
+    CK(cudaSetDevice(ctx->dev));
+    int r = ensure_halo(ctx);
+    if (r) return r;
+    const HaloDesc d = halo_desc(ctx, which, true);
+    long long tot = 0;
+    for (int s = 0; s < 8; ++s) tot += (long long)d.cells[s] * d.width;
+    if (!tot) return MM2D_OK;
+    k_halo_pack<<<grid_for(tot / 4 + 1, 256), 256, 0, (cudaStream_t)stream>>>(
+        ctx->g, which, d_src, ctx->d_Hr, d);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    return MM2D_OK;
 }
+
 extern "C" int mm2d_halo_unpack(mm2d_ctx* ctx, int which, void* stream) {
-    (void)which; (void)stream;
-    return fail_cfg(ctx, "halo exchange buffers are not enabled in this build");
+    if (!ctx || which < 0 || which > 2) return fail_cfg(ctx, "bad halo field");
+    CK(cudaSetDevice(ctx->dev));
+    int r = ensure_halo(ctx);
+    if (r) return r;
+    if (which == 0) return MM2D_OK;   // G is received in place
+    const HaloDesc d = halo_desc(ctx, which, false);
+    long long tot = 0;
+    for (int s = 0; s < 8; ++s) tot += (long long)d.cells[s] * d.width;
+    if (!tot) return MM2D_OK;
+    k_halo_unpack<<<grid_for(tot, 256), 256, 0, (cudaStream_t)stream>>>(
+        ctx->g, which == 1 ? ctx->d_Qr : ctx->d_Hr, d);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    return MM2D_OK;
 }
 
 // ---------------------------------------------------------------------------

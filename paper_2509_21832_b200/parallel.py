@@ -1,0 +1,330 @@
+"""Block domain decomposition of the 2D step across GPUs.
+
+Drop-in for the reference's worker-grid runner
+(pkg/src/micromacro/runner/parallel.py): ``HaloPlan`` / ``make_plans``
+(50-93) partition the (nx, ny) grid into a rows x cols block grid with the
+same rank numbering and periodic neighbour wrap; ``run_parallel_2d``
+(404-473) keeps its signature and return value.
+
+Where the reference forks CPU workers that read one-cell rings straight out
+of POSIX shared memory (extract_ring, 109-150) and meet at two barriers per
+step (384-394), each block here is a libmm2d context on a GPU and the rings
+are exchanged explicitly, twice per step, exactly at the reference's two
+barrier points:
+
+  1. before the micro phase: the G ring (V doubles per cell) and the Q ring
+     (6 doubles per cell) from up to 8 neighbours (faces + corners);
+  2. between the micro and the macro phase: the heat-tensor ring (4 doubles
+     per cell).
+
+Two transports implement the same slot protocol (slot s of a block goes to
+its neighbour in direction s and lands in that neighbour's slot opposite(s)):
+
+  * ``DistExchange``: one process per GPU, ``torch.distributed`` batched
+    isend/irecv -- NCCL over NVLink/NVSwitch on B200, gloo on CPU (tests);
+  * ``LoopbackExchange``: all blocks in one process, device-to-device copies
+    between the contexts' staging buffers (peer copies when the blocks sit
+    on different GPUs).
+
+Per-cell arithmetic does not depend on the decomposition, so results are
+bitwise identical to the single-block step (the property the reference's
+test_parallel.py:96-110 pins for its worker grid).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .boundary import PERIODIC
+from .errors import ConfigurationError
+
+# slot order shared with the C ABI (include/mm2d.h): faces then corners
+SLOTS = ("left", "right", "bottom", "top", "bottom_left", "bottom_right", "top_left",
+         "top_right")
+SLOT_DIR = ((-1, 0), (1, 0), (0, -1), (0, 1), (-1, -1), (1, -1), (-1, 1), (1, 1))
+OPPOSITE = (1, 0, 3, 2, 7, 6, 5, 4)
+FIELD_G, FIELD_Q, FIELD_H = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class HaloPlan:
+    """One block's extent and its exchange neighbours (rank per slot, None
+    for a physical face or a face wrapped locally)."""
+
+    rank: int
+    grid: tuple
+    pos: tuple
+    i0: int
+    i1: int
+    j0: int
+    j1: int
+    neighbors: dict          # face name -> rank or None (reference naming)
+    slots: tuple             # 8 entries: neighbour rank per exchange slot
+
+    @property
+    def shape(self):
+        return (self.i1 - self.i0, self.j1 - self.j0)
+
+
+def make_plans(nx, ny, grid, bc):
+    """Block plans in the reference's numbering: rank = r * cols + c for
+    block (r, c), x split into `rows`, y into `cols` (parallel.py:69-93)."""
+    rows, cols = grid
+    if rows < 1 or cols < 1 or nx % rows != 0 or ny % cols != 0:
+        raise ConfigurationError(
+            f"worker grid {rows}x{cols} must divide the spatial grid {nx}x{ny}")
+    bx, by = nx // rows, ny // cols
+    xper = bc.left == PERIODIC
+    yper = bc.bottom == PERIODIC
+
+    def nb_face(r, c, dr, dc):
+        rr, cc = r + dr, c + dc
+        if 0 <= rr < rows and 0 <= cc < cols:
+            return rr * cols + cc
+        if dr and xper:
+            return (rr % rows) * cols + cc
+        if dc and yper:
+            return rr * cols + (cc % cols)
+        return None
+
+    plans = []
+    for r in range(rows):
+        for c in range(cols):
+            faces = {"left": nb_face(r, c, -1, 0), "right": nb_face(r, c, 1, 0),
+                     "bottom": nb_face(r, c, 0, -1), "top": nb_face(r, c, 0, 1)}
+            # exchange slots: a face is exchanged iff it is an interior face or
+            # periodic across more than one block along that axis (a single
+            # block wraps locally); corners iff both adjacent faces are
+            xs = [faces["left"] if (r > 0 or (xper and rows > 1)) else None,
+                  faces["right"] if (r < rows - 1 or (xper and rows > 1)) else None]
+            ys = [faces["bottom"] if (c > 0 or (yper and cols > 1)) else None,
+                  faces["top"] if (c < cols - 1 or (yper and cols > 1)) else None]
+            slot = xs + ys
+            for dr, dc in SLOT_DIR[4:]:
+                ok = slot[0 if dr < 0 else 1] is not None and slot[2 if dc < 0 else 3] is not None
+                slot.append(((r + dr) % rows) * cols + ((c + dc) % cols) if ok else None)
+            plans.append(HaloPlan(rank=r * cols + c, grid=(rows, cols), pos=(r, c),
+                                  i0=r * bx, i1=(r + 1) * bx, j0=c * by, j1=(c + 1) * by,
+                                  neighbors=faces, slots=tuple(slot)))
+    return plans
+
+
+# ---------------------------------------------------------------------------
+# transports
+# ---------------------------------------------------------------------------
+
+class DistExchange:
+    """Slot exchange over torch.distributed point-to-point (one block per
+    rank).  ``bufs[field][slot] = (send, recv)`` tensors (None when the slot
+    is inactive).  Sends are posted in slot order and receives in slot order
+    of the opposite direction, so the matching between any pair of ranks is
+    well defined even when one neighbour occupies several slots (periodic
+    wrap over two blocks)."""
+
+    def __init__(self, plan: HaloPlan, bufs, group=None):
+        self.plan = plan
+        self.bufs = bufs
+        self.group = group
+
+    def exchange(self, field):
+        import torch.distributed as dist
+        ops = []
+        for s in range(8):
+            peer = self.plan.slots[s]
+            send, _ = self.bufs[field][s]
+            if peer is not None and send is not None:
+                ops.append(dist.P2POp(dist.isend, send, peer, self.group))
+        for s in range(8):
+            o = OPPOSITE[s]
+            peer = self.plan.slots[o]
+            _, recv = self.bufs[field][o]
+            if peer is not None and recv is not None:
+                ops.append(dist.P2POp(dist.irecv, recv, peer, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+
+class LoopbackExchange:
+    """Slot exchange between blocks held by one process: copy every active
+    send slot into the neighbour's opposite receive slot."""
+
+    def __init__(self, plans, bufs_per_block):
+        self.plans = plans
+        self.bufs = bufs_per_block
+
+    def exchange(self, field):
+        for p in self.plans:
+            for s in range(8):
+                peer = p.slots[s]
+                if peer is None:
+                    continue
+                send, _ = self.bufs[p.rank][field][s]
+                _, recv = self.bufs[peer][field][OPPOSITE[s]]
+                if send is not None and recv is not None:
+                    recv.copy_(send, non_blocking=True)
+
+
+# ---------------------------------------------------------------------------
+# device blocks
+# ---------------------------------------------------------------------------
+
+class _CAI:
+    """Minimal __cuda_array_interface__ view of a device pointer."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def halo_buffers(solver):
+    """(send, recv) tensors per (field, slot), viewing the context's staging
+    buffers (None for inactive slots)."""
+    import torch
+    lib, ctx = solver.lib, solver.ctx
+    out = []
+    for f in range(3):
+        row = []
+        for s in range(8):
+            sp, rp, n = C.c_void_p(), C.c_void_p(), C.c_longlong()
+            rc = lib.mm2d_halo_info(ctx, f, s, C.byref(sp), C.byref(rp), C.byref(n))
+            if rc != 0:
+                raise RuntimeError(f"mm2d_halo_info failed: {rc}")
+            if n.value == 0:
+                row.append((None, None))
+                continue
+            with torch.cuda.device(solver.device):
+                st = torch.as_tensor(_CAI(sp.value, n.value), device=solver.device)
+                rt = torch.as_tensor(_CAI(rp.value, n.value), device=solver.device)
+            row.append((st, rt))
+        out.append(row)
+    return out
+
+
+class BlockStepper:
+    """One block of a decomposition on one GPU: a libmm2d context plus the
+    exchange protocol around its two step phases."""
+
+    def __init__(self, mesh, bc, eps, model, grid, plan: HaloPlan, device):
+        from .solver import Solver2D
+        self.plan = plan
+        self.solver = Solver2D(mesh, bc, eps, model, grid=grid, rank=plan.pos, device=device)
+        self.bufs = halo_buffers(self.solver)
+
+    def _stream(self):
+        import torch
+        return C.c_void_p(torch.cuda.current_stream(self.solver.device).cuda_stream)
+
+    def pack(self, field, src):
+        s = self.solver
+        rc = s.lib.mm2d_halo_pack(s.ctx, field, C.c_void_p(0 if src is None else src.data_ptr()),
+                                  self._stream())
+        s._rc(rc)
+
+    def unpack(self, field):
+        s = self.solver
+        s._rc(s.lib.mm2d_halo_unpack(s.ctx, field, self._stream()))
+
+    def phase(self, ph, Q, G, dt, Qout, Gout, H):
+        s = self.solver
+        from .solver import _ptr
+        rc = s.lib.mm2d_step_phase(s.ctx, ph, _ptr(Q), _ptr(G), C.c_double(dt), _ptr(Qout),
+                                   _ptr(Gout), _ptr(H), 0, None, None, None, self._stream())
+        s._rc(rc)
+
+
+def step_blocks(blocks, exchange, states, dt):
+    """One decomposed step for every block held by this process.
+    ``states[b] = (Q, G, Qout, Gout, H)`` device tensors of block b."""
+    import torch
+    for b, st in zip(blocks, states):
+        with torch.cuda.device(b.solver.device):
+            b.pack(FIELD_G, st[1])
+            b.pack(FIELD_Q, st[0])
+    _sync_devices(blocks)
+    exchange.exchange(FIELD_G)
+    exchange.exchange(FIELD_Q)
+    _sync_devices(blocks)
+    for b, st in zip(blocks, states):
+        with torch.cuda.device(b.solver.device):
+            b.unpack(FIELD_Q)
+            b.phase(0, st[0], st[1], dt, st[2], st[3], st[4])
+            b.pack(FIELD_H, None)
+    _sync_devices(blocks)
+    exchange.exchange(FIELD_H)
+    _sync_devices(blocks)
+    for b, st in zip(blocks, states):
+        with torch.cuda.device(b.solver.device):
+            b.unpack(FIELD_H)
+            b.phase(1, st[0], st[1], dt, st[2], st[3], st[4])
+
+
+def _sync_devices(blocks):
+    """Order cross-device copies after the producing kernels (loopback over
+    several GPUs); a no-op cost when every block shares one device."""
+    import torch
+    devs = sorted({b.solver.device.index for b in blocks})
+    if len(devs) > 1:
+        for d in devs:
+            torch.cuda.synchronize(d)
+
+
+def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), track_from=None,
+                    devices=None):
+    """Advance n_steps with a rows x cols block grid spread over the visible
+    GPUs (blocks round-robin over ``devices``); returns
+    (Q, G, steady_max, seconds) like the reference (parallel.py:404-473).
+    steady_max is the largest per-step max-norm change of Q over steps
+    >= track_from (NaN if untracked); seconds is the wall time of the
+    stepping loop (device-synchronised, excluding setup and gathers)."""
+    import torch
+    nx, ny = mesh.space[0].n, mesh.space[1].n
+    plans = make_plans(nx, ny, grid, bc)
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    blocks, states = [], []
+    Q0 = np.asarray(Q0, dtype=np.float64)
+    G0 = np.asarray(G0, dtype=np.float64)
+    for p in plans:
+        dev = torch.device("cuda", devices[p.rank % len(devices)])
+        b = BlockStepper(mesh, bc, eps, model, grid, p, dev)
+        blocks.append(b)
+        Q = torch.from_numpy(np.ascontiguousarray(Q0[p.i0:p.i1, p.j0:p.j1])).to(dev)
+        G = torch.from_numpy(np.ascontiguousarray(G0[p.i0:p.i1, p.j0:p.j1])).to(dev)
+        H = torch.empty((4,) + p.shape, dtype=torch.float64, device=dev)
+        states.append([Q, G, torch.empty_like(Q), torch.empty_like(G), H])
+    exchange = LoopbackExchange(plans, [b.bufs for b in blocks])
+    steady = 0.0
+    for d in devices:
+        torch.cuda.synchronize(d)
+    t0 = time.perf_counter()
+    for n in range(n_steps):
+        step_blocks(blocks, exchange, states, dt)
+        if track_from is not None and n >= track_from:
+            for st in states:
+                steady = max(steady, float((st[2] - st[0]).abs().max()))
+        for st in states:
+            st[0], st[2] = st[2], st[0]
+            st[1], st[3] = st[3], st[1]
+    for d in devices:
+        torch.cuda.synchronize(d)
+    seconds = time.perf_counter() - t0
+    for b in blocks:
+        b.solver.check()
+    Q = np.empty_like(Q0)
+    G = np.empty_like(G0)
+    for p, st in zip(plans, states):
+        Q[p.i0:p.i1, p.j0:p.j1] = st[0].cpu().numpy()
+        G[p.i0:p.i1, p.j0:p.j1] = st[1].cpu().numpy()
+    for b in blocks:
+        b.solver.close()
+    return Q, G, (steady if track_from is not None else float("nan")), seconds
+
+
+__all__ = ["HaloPlan", "make_plans", "DistExchange", "LoopbackExchange", "BlockStepper",
+           "halo_buffers", "step_blocks", "run_parallel_2d", "SLOTS", "OPPOSITE"]

@@ -83,6 +83,8 @@ class Solver2D:
         self.lib = _native.load()
         if device is None:
             device = torch.cuda.current_device()
+        if isinstance(device, torch.device):
+            device = device.index if device.index is not None else torch.cuda.current_device()
         self.device = torch.device("cuda", int(device))
         self.mesh, self.bc, self.eps, self.model = mesh, bc, float(eps), model
         self.grid, self.rank = tuple(grid), tuple(rank)

@@ -228,3 +228,52 @@ def test_full_size_c2_conservation(mm):
     inv1 = [Qf[..., 0].sum(), Qf[..., 1].sum(), Qf[..., 2].sum(), (Qf[..., 3] + Qf[..., 5]).sum()]
     for a, b in zip(inv0, inv1):
         assert abs(a - b) <= 1e-11 * abs(a)
+
+
+# -- block decomposition (reference test_parallel.py:96-128) ---------------
+
+def _parallel_problem(nx, ny, nv, faces, seed):
+    from paper_2509_21832_b200 import (Axis, BoundarySpec2D, CollisionModel, PhaseMesh,
+                                       conserved_2d)
+    mesh = PhaseMesh(space=(Axis(0.0, 1.0, nx), Axis(0.0, 1.0, ny)),
+                     velocity=(Axis(-5.0, 5.0, nv), Axis(-5.0, 5.0, nv)))
+    x = (np.arange(nx) + 0.5) / nx
+    y = (np.arange(ny) + 0.5) / ny
+    X, Y = np.meshgrid(x, y, indexing="ij")
+    rho = 1.0 + 0.2 * np.sin(2 * np.pi * X) * np.cos(2 * np.pi * Y)
+    T = 1.0 + 0.1 * np.cos(2 * np.pi * X)
+    Q = conserved_2d(rho, 0.02 * np.cos(2 * np.pi * Y), -0.03 * np.sin(2 * np.pi * X), T,
+                     0.02 * np.sin(2 * np.pi * (X + Y)), T)
+    G = 0.01 * np.random.default_rng(seed).standard_normal((nx, ny, nv, nv))
+    return mesh, BoundarySpec2D(*faces), CollisionModel("esbgk_2d", nu=-0.5), Q, G
+
+
+@pytest.mark.parametrize("nv", [6, 32])
+@pytest.mark.parametrize("grid,faces", [
+    ((2, 2), "cavity"), ((3, 4), "cavity"), ((2, 2), "periodic"), ((4, 3), "mixed"),
+    ((1, 1), "periodic"), ((2, 1), "periodic"), ((1, 3), "cavity")])
+def test_block_grid_equals_serial_bitwise(mm, grid, faces, nv):
+    from paper_2509_21832_b200 import EXTRAPOLATE, PERIODIC, WallSpec
+    from paper_2509_21832_b200.parallel import run_parallel_2d
+    w = WallSpec(1.0)
+    fc = {"cavity": (w, w, w, WallSpec(1.0, 0.16)), "periodic": (PERIODIC,) * 4,
+          "mixed": (EXTRAPOLATE, EXTRAPOLATE, PERIODIC, PERIODIC)}[faces]
+    mesh, bc, model, Q0, G0 = _parallel_problem(12, 12, nv, fc, 11)
+    dt = 0.3 * (1.0 / 12) / 5.0
+    Qp, Gp, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, 6, grid=grid)
+    st = mm.State2D(0.0, Q0, G0)
+    for _ in range(6):
+        st = mm.step_2d(st, mesh, bc, 0.08, model, dt)
+    assert np.array_equal(Qp, st.Q)
+    assert np.array_equal(Gp, st.G)
+
+
+def test_block_grid_steady_tracking(mm):
+    from paper_2509_21832_b200 import PERIODIC
+    from paper_2509_21832_b200.parallel import run_parallel_2d
+    mesh, bc, model, Q0, G0 = _parallel_problem(8, 8, 6, (PERIODIC,) * 4, 3)
+    Q, G, smax, secs = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, 1e-3, 4, grid=(2, 2),
+                                       track_from=2)
+    assert np.isfinite(smax) and smax > 0.0 and secs > 0.0
+    _, _, snan, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, 1e-3, 2, grid=(2, 2))
+    assert np.isnan(snan)
