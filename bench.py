@@ -67,8 +67,11 @@ def make_workload(name, n_gpus=1, px=1, py=1):
     if name == "c2":
         n, v, faces, eps, ic = 256, (-7.0, 7.0), "periodic", 0.1, "wave"
         wl = "C2 smooth periodic density wave 256^2 x 32^2 (BASELINE configs[1])"
-        nx = ny = n
-        Lx = Ly = 1.0
+        if px * py > 1:
+            wl = (f"C2 weak scaling: 256^2 x 32^2 per GPU, periodic wave tiled on "
+                  f"{px}x{py} GPUs ({256 * px}x{256 * py} cells)")
+        nx, ny = n * px, n * py
+        Lx, Ly = float(px), float(py)
     elif name == "c3":
         nx = ny = 512
         v, faces, eps, ic = (-8.0, 8.0), "extrapolate", 1e-2, "riemann"
@@ -84,7 +87,7 @@ def make_workload(name, n_gpus=1, px=1, py=1):
         v, faces, eps, ic = (-7.0, 7.0), "periodic", 1e-2, "fourier"
         wl = "C5 strong-scaling 2048^2 x 32^2 periodic random Fourier, eps=1e-2"
         Lx = Ly = 1.0
-    elif name == "weak":
+    elif name in ("weak", "c5w"):
         nx, ny = 1024 * px, 1024 * py
         v, faces, eps, ic = (-7.0, 7.0), "periodic", 1e-2, "fourier"
         wl = f"C5 weak scaling 1024^2 x 32^2 per GPU ({nx}x{ny} total)"
@@ -287,7 +290,135 @@ def run_reference_arm(args, rank, world):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+RANK_GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
+
+
+def rank_grid(world):
+    if world in RANK_GRIDS:
+        return RANK_GRIDS[world]
+    px = int(math.sqrt(world))
+    while world % px:
+        px -= 1
+    return (world // px, px)
+
+
+def run_ours_multi(args, rank, world, local_rank):
+    """Weak scaling over `world` GPUs (one process each): the N=1 workload's
+    block per GPU, tiled into a px x py block grid of one periodic domain,
+    with the two NCCL halo exchanges per step (G+Q ring, heat ring)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2509_21832_b200 import _native
+    from paper_2509_21832_b200.parallel import (BlockStepper, DistExchange, make_plans,
+                                                step_blocks)
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    px, py = rank_grid(world)
+    cfg_name = args.config or "c2"
+    cfg = make_workload(cfg_name, px=px, py=py)
+    nx, ny, V = cfg["nx"], cfg["ny"], cfg["V"]
+    plan = make_plans(nx, ny, (px, py), cfg["bc"])[rank]
+    blk = BlockStepper(cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"], (px, py), plan,
+                       torch.device("cuda", local_rank))
+    exch = DistExchange(plan, blk.bufs)
+    lib = _native.load()
+    bx, by = plan.shape
+    Q = torch.from_numpy(cfg["initial"](plan.i0, plan.i1, plan.j0, plan.j1)).cuda()
+    G = torch.zeros((bx, by, 32, 32), dtype=torch.float64, device="cuda")
+    st = [Q, G, torch.empty_like(Q), torch.empty_like(G),
+          torch.empty((4, bx, by), dtype=torch.float64, device="cuda")]
+    dt = cfg["dt"]
+    dist.barrier()
+
+    def steps(n):
+        for _ in range(n):
+            step_blocks([blk], exch, [st], dt)
+            st[0], st[2] = st[2], st[0]
+            st[1], st[3] = st[3], st[1]
+
+    steps(args.warmup)
+    torch.cuda.synchronize()
+    blk.solver.check()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize()
+    lib.mm2d_reset_launch_count()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tw0 = time.time()
+    e0.record(stream)
+    steps(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    launches = int(lib.mm2d_launch_count())
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    dist.barrier()
+    time.sleep(0.2)
+    clocks.stop()
+    blk.solver.check()
+    clk = clocks.summary(tw0 - 0.05, tw1 + 0.05)
+    value = nx * ny * V * args.steps / (ms / 1e3)
+    ms_step = ms / args.steps
+    peak, peak_src = measured_peak()
+    step_bytes = bytes_per_step(nx, ny, V)
+    step_gbs = step_bytes / (ms_step / 1e3) / 1e9
+    # end to end: every rank uploads its block from pinned host memory,
+    # runs one decomposed step and downloads the result
+    Qh = st[0].cpu().pin_memory()
+    Gh = st[1].cpu().pin_memory()
+    Qo, Go = torch.empty_like(Qh).pin_memory(), torch.empty_like(Gh).pin_memory()
+    Ho = torch.empty((4, bx, by), dtype=torch.float64).pin_memory()
+    n_e2e = max(3, min(args.steps, 10))
+    dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(n_e2e):
+        st[0].copy_(Qh, non_blocking=True)
+        st[1].copy_(Gh, non_blocking=True)
+        step_blocks([blk], exch, [st], dt)
+        Qo.copy_(st[2], non_blocking=True)
+        Go.copy_(st[3], non_blocking=True)
+        Ho.copy_(st[4], non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([f0.elapsed_time(f1) / n_e2e], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE config initial conditions, g=0)",
+        "config": {"workload": cfg["workload"], "nx": nx, "ny": ny, "nv1": 32, "nv2": 32,
+                   "dt": dt, "parallelism": f"dd{px}x{py}",
+                   "exchange": "NCCL send/recv (torch.distributed), G+Q ring and heat ring per step",
+                   "l2": "inputs larger than L2 (G per GPU = %.0f MiB)" % (bx * by * V * 8 / 2**20)},
+        "roofline": {"bound": "hbm", "kernel": "full decomposed step",
+                     "achieved": step_gbs / world, "peak": peak, "unit": "GB/s",
+                     "frac": step_gbs / world / peak, "traffic": None, "peak_source": peak_src,
+                     "note": "per-GPU algorithmic bytes of the whole step / step time"},
+        "e2e": {"value": nx * ny * V / (e2e_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": 8 * bx * by * (6 + V) * world,
+                "d2h_bytes_per_step": 8 * bx * by * (6 + V + 4) * world, "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def run_ours(args, rank, world, local_rank):
+    if world > 1:
+        return run_ours_multi(args, rank, world, local_rank)
     import torch
     import paper_2509_21832_b200 as mm
     from paper_2509_21832_b200 import _native
@@ -295,10 +426,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    cfg_name = args.config or ("c2" if world == 1 else "weak")
+    cfg_name = args.config or "c2"
     cfg = make_workload(cfg_name)
     lib = _native.load()
     solver = Solver2D(cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"])
@@ -345,7 +473,7 @@ def run_ours(args, rank, world, local_rank):
     solver.check()
     clk = clocks.summary(tw0 - 0.05, tw1 + 0.05)
 
-    nodes = nx * ny * V * args.steps * (world if cfg_name != "weak" else 1)
+    nodes = nx * ny * V * args.steps
     value = nodes / (ms / 1e3)
     ms_step = ms / args.steps
 
