@@ -42,6 +42,7 @@ struct mm2d_ctx {
     double* d_zero = nullptr;      // V zeros
     bool use32 = false;            // specialised 32 x 32 micro kernel
     int grid32 = 1;                // persistent CTAs of k_micro32
+    int np32 = 4;                  // node pairs per thread of k_micro32
     int ly32 = 32;
     // context-owned state
     double* d_Qs[2] = {nullptr, nullptr};
@@ -226,19 +227,25 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         }
     }
     if (ctx->use32) {
-        if (cudaFuncSetAttribute(reinterpret_cast<const void*>(&m32::k_micro32),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)m32::smem_bytes_v3()) != cudaSuccess) {
+        const char* np = getenv("MM2D_NP");
+        ctx->np32 = np ? atoi(np) : 4;
+        if (ctx->np32 != 2 && ctx->np32 != 8) ctx->np32 = 4;
+        const void* fn = ctx->np32 == 2 ? reinterpret_cast<const void*>(&m32::k_micro32<2>)
+                         : ctx->np32 == 8 ? reinterpret_cast<const void*>(&m32::k_micro32<8>)
+                                          : reinterpret_cast<const void*>(&m32::k_micro32<4>);
+        const size_t sm = ctx->np32 == 2 ? m32::smem_bytes_v3<2>()
+                          : ctx->np32 == 8 ? m32::smem_bytes_v3<8>() : m32::smem_bytes_v3<4>();
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm) != cudaSuccess) {
             int r = fail_cfg(ctx, "shared memory request too large for k_micro32");
             delete ctx;
             return r;
         }
         int occ = 0, nsm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, m32::k_micro32, m32::NT,
-                                                      m32::smem_bytes_v3());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 512 / ctx->np32, sm);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
         const char* ly = getenv("MM2D_LY");
-        ctx->ly32 = ly ? std::max(1, atoi(ly)) : 32;
+        ctx->ly32 = ly ? std::max(1, atoi(ly)) : 48;
         ctx->ly32 = std::min(ctx->ly32, g.by);
         const long long items = (long long)((g.by + ctx->ly32 - 1) / ctx->ly32) * g.bx;
         const char* pe = getenv("MM2D_PERSIST");
@@ -403,7 +410,12 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
         }
         ma.ly = ctx->ly32;
         dim3 grid(g.bx, (g.by + ctx->ly32 - 1) / ctx->ly32);
-        m32::k_micro32<<<grid, m32::NT, m32::smem_bytes_v3(), s>>>(ma);
+        if (ctx->np32 == 2)
+            m32::k_micro32<2><<<grid, 256, m32::smem_bytes_v3<2>(), s>>>(ma);
+        else if (ctx->np32 == 8)
+            m32::k_micro32<8><<<grid, 64, m32::smem_bytes_v3<8>(), s>>>(ma);
+        else
+            m32::k_micro32<4><<<grid, 128, m32::smem_bytes_v3<4>(), s>>>(ma);
     } else {
         dim3 grid((g.bx + ctx->BX - 1) / ctx->BX, (g.by + ctx->ly - 1) / ctx->ly);
         void* args[] = {&ma};

@@ -32,15 +32,15 @@ namespace m32 {
 
 constexpr int NV = 32;
 constexpr int V = NV * NV;
-constexpr int NT = 128;
-constexpr int NP = 4;                // node pairs per thread
+constexpr int NT = 128;              // threads of the default 8-node (NP = 4) variant
+constexpr int NP = 4;                // node pairs per thread (default variant)
 constexpr int TSLOTS = 5;            // table slots (rows j..j+3 + WAR margin)
 constexpr int KT = 0;                // K-table [32][8]
 constexpr int LT = KT + 8 * NV;      // L-table [8][32]
 constexpr int GK = LT + 8 * NV;      // Gaussian k-table [32][2] (GA, GD)
 constexpr int GL = GK + 2 * NV;      // Gaussian l-table [2][32] (GB, GR)
 constexpr int TAB = GL + 2 * NV;     // 640 doubles per cell
-enum { K_PE1, K_W1N, K_H1, K_W1, K_U, K_C, K_Q1, K_P1 };
+enum { K_W1N, K_H1, K_PE1, K_W1, K_U, K_C, K_Q1, K_P1 };   // pairs: (w1,h1) (pE1,W1) (U,c) (q1,p1)
 enum { L_E2, L_W2N, L_H2, L_W2, L_V, L_Q2, L_P2 };
 
 inline size_t smem_bytes() {
@@ -133,32 +133,57 @@ __device__ __forceinline__ double fexp(double x) {
 // stores), 96 threads each add 16 partials of one value (rotated start so a
 // warp's 16-byte loads hit 8 distinct bank groups), 8-lane shuffles finish,
 // and all threads read the 12 totals back.  Two barriers, ~50 instructions.
-constexpr int RED = 12 * NT + 16;    // doubles of reduction scratch
+// tree sum of a per-pair contribution array
+template <int N>
+__device__ __forceinline__ double tsum(const double (&c)[N]) {
+    if constexpr (N == 8) return ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]));
+    else if constexpr (N == 4) return (c[0] + c[1]) + (c[2] + c[3]);
+    else if constexpr (N == 2) return c[0] + c[1];
+    else return c[0];
+}
 
-__device__ __forceinline__ void reduce12(double (&v)[12], double* sred) {
-    const int tid = threadIdx.x;
+template <int NT_> constexpr int red_size() { return 12 * NT_ + 16; }   // doubles
+
+// phase A: store partials, barrier.  phase B + totals: reduce12_end.  Work
+// that touches neither the partials nor the totals may sit in between.
+template <int NT_>
+__device__ __forceinline__ void reduce12_begin(const double (&v)[12], double* sred) {
 #pragma unroll
-    for (int q = 0; q < 12; ++q) sred[q * NT + tid] = v[q];
+    for (int q = 0; q < 12; ++q) sred[q * NT_ + threadIdx.x] = v[q];
     __syncthreads();
-    if (tid < 96) {
-        const int vid = tid >> 3, seg = tid & 7;
-        const double* src = sred + vid * NT + 16 * seg;
-        double2 x[8];
+}
+
+template <int NT_>
+__device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
+    constexpr int NS = NT_ >= 128 ? 8 : 4;  // segments per value (threads per value)
+    constexpr int SEG = NT_ / NS;           // partials per (value, segment)
+    constexpr int L2N = SEG / 2;            // double2 loads per segment
+    const int tid = threadIdx.x;
+    // whole warps take part so the shuffles below are well defined
+    if ((tid & ~31) < 12 * NS) {
+        const bool act = tid < 12 * NS;
+        const int vid = act ? tid / NS : 0, seg = tid % NS;
+        const double* src = sred + vid * NT_ + SEG * seg;
+        double u[L2N];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) x[q] = lds2(src + 2 * ((q + seg) & 7));
-        double u[8];
+        for (int q = 0; q < L2N; ++q) {
+            const double2 x = lds2(src + 2 * ((q + seg) & (L2N - 1)));
+            u[q] = x.x + x.y;
+        }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) u[q] = x[q].x + x[q].y;
-        double acc = ((u[0] + u[1]) + (u[2] + u[3])) + ((u[4] + u[5]) + (u[6] + u[7]));
-        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        for (int w = 1; w < L2N; w <<= 1)
+#pragma unroll
+            for (int q = 0; q < L2N; q += 2 * w) u[q] += u[q + w];
+        double acc = u[0];
+        if (NS == 8) acc += __shfl_xor_sync(0xffffffffu, acc, 4);
         acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (seg == 0) sred[12 * NT + vid] = acc;
+        if (act && seg == 0) sred[12 * NT_ + vid] = acc;
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 12; q += 2) {
-        const double2 x = lds2(sred + 12 * NT + q);
+        const double2 x = lds2(sred + 12 * NT_ + q);
         v[q] = x.x;
         v[q + 1] = x.y;
     }
@@ -167,9 +192,10 @@ __device__ __forceinline__ void reduce12(double (&v)[12], double* sred) {
 // build the per-cell tables from the shared copy P of the cell's CellPar.
 // Work split so every warp does the same number of exps: warp 0 the K-table
 // (+ GD), warp 1 the L-table (+ GR), warps 2/3 the Gaussian GA / GB.
+template <int KS>
 __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, const CellPar& P,
                                              const double* v1s, const double* v2s, bool gauss) {
-    const int t = threadIdx.x;
+    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
     const int m = t & 31;
     if (t < 32) {
         const double W1 = v1s[m] - P.u1;
@@ -178,8 +204,8 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         const double q1 = W1s * P.inv2T - 2.0;
         const double p1 = W1 * P.gT1 * P.invT;
         double* K = T + KT + 8 * m;
-        sts2(K + K_PE1, P.pref * fexp(-W1s * P.inv2T), w1);
-        sts2(K + K_H1, 0.5 * w1 * w1 - 1.0, W1);
+        sts2(K + K_W1N, w1, 0.5 * w1 * w1 - 1.0);
+        sts2(K + K_PE1, P.pref * fexp(-W1s * P.inv2T), W1);
         sts2(K + K_U, W1s * P.s11 * P.inv2T + q1 * p1, 2.0 * W1 * P.s12 * P.inv2T);
         sts2(K + K_Q1, q1, p1);
         if (gauss) T[GK + 2 * m + 1] = fexp(P.gq12 * W1 * (v2s[1] - v2s[0]));
@@ -202,13 +228,14 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         L[L_V * NV] = q2 * p2 - W2s * P.s11 * P.inv2T;
         L[L_Q2 * NV] = q2;
         L[L_P2 * NV] = p2;
-        if (gauss) T[GL + NV + m] = fexp(P.gq12 * (v1s[8] - v1s[0]) * W2);
+        if (gauss) T[GL + NV + m] = fexp(P.gq12 * (v1s[KS] - v1s[0]) * W2);
     } else if (gauss && t < 96) {
         const double W1 = v1s[m] - P.u1;
         T[GK + 2 * m] = P.gpref * a.inveps * P.wh * fexp(P.gq11 * (W1 * W1));
     } else if (gauss) {
         const double W2 = v2s[m] - P.u2;
         T[GL + m] = fexp(P.gq22 * (W2 * W2));
+    }
     }
 }
 
@@ -221,15 +248,20 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
+template <int NP_>
 inline size_t smem_bytes_v3() {
-    return sizeof(double) * (3 * V + TSLOTS * SLOT + RED + 4 * 32 + 2 * NV + 2 * NP * NT);
+    constexpr int NT_ = 512 / NP_;
+    return sizeof(double) * (3 * V + TSLOTS * SLOT + red_size<NT_>() + 4 * 32 + 2 * NV + 2 * NP_ * NT_);
 }
 
 // The host selects this kernel only when the velocity axes make the upwind
 // direction a compile-time property of the node pair: v1 < 0 exactly for
 // k < 16 (pairs p = 0, 1 difference towards the right neighbour), and both
 // nodes of every (l, l+1) pair share the sign of v2.
-__global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
+template <int NP_>
+__global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_micro32(MicroArgs a) {
+    constexpr int NT_ = 512 / NP_;       // threads per CTA
+    constexpr int KS = 32 / NP_;         // k step between a thread's node pairs
     extern __shared__ __align__(16) double smem[];
     const Geometry& g = a.g;
     if (*a.err != kNoError) return;
@@ -239,7 +271,7 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
     double* ring = smem;                            // [3][V]
     double* tabs = ring + 3 * V;                    // [TSLOTS][SLOT]
     double* sred = tabs + TSLOTS * SLOT;            // [12][NT] partials + [12] totals
-    double* pring = sred + RED;                     // [4][32] staged CellPar rows
+    double* pring = sred + red_size<NT_>();                     // [4][32] staged CellPar rows
     double* v1s = pring + 4 * 32;
     double* v2s = v1s + NV;
     if (tid < NV) v1s[tid] = a.v1[tid];
@@ -258,12 +290,12 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
     // koff(p) = koff0 + 64 p into the K-table (immediate offsets in SASS)
     const int off0 = 32 * kb + lb;
     const int koff0 = KT + 8 * kb;
-#define off_(p) (off0 + 256 * (p))
-#define koff_(p) (koff0 + 64 * (p))
-    double cx[NP];
+#define off_(p) (off0 + 32 * KS * (p))
+#define koff_(p) (koff0 + 8 * KS * (p))
+    double cx[NP_];
 #pragma unroll
-    for (int p = 0; p < NP; ++p)
-        cx[p] = (p < 2 ? -a.dt : a.dt) * v1s[kb + 8 * p] * a.idx;
+    for (int p = 0; p < NP_; ++p)
+        cx[p] = (p < NP_ / 2 ? -a.dt : a.dt) * v1s[kb + KS * p] * a.idx;
     const bool negy = v2s[lb] < 0.0;
     const double sy = negy ? -a.dt : a.dt;
     const double cy0 = sy * v2s[lb] * a.idy, cy1 = sy * v2s[lb + 1] * a.idy;
@@ -324,7 +356,7 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
     cp_async_wait_all();
     __syncthreads();
 
-    double2 pf[NP];               // prefetched own G^n of the next x-stage row
+    double2 pf[NP_];               // prefetched own G^n of the next x-stage row
     double* hst = pring + 4 * 32 + 2 * NV;   // [NP][NT] double2 halo staging (thread-private)
     auto prefetch = [&](int r) {
         const double *own, *hl, *hr;
@@ -341,9 +373,9 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
             if (!hr) hr = a.zero;
         }
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
+        for (int p = 0; p < NP_; ++p) {
             pf[p] = __ldg(reinterpret_cast<const double2*>(own + off_(p)));
-            cp_async16(hst + 2 * (p * NT + tid), (p < 2 ? hr : hl) + off_(p));
+            cp_async16(hst + 2 * (p * NT_ + tid), (p < NP_ / 2 ? hr : hl) + off_(p));
         }
         cp_async_commit();
     };
@@ -361,19 +393,16 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
 
     double ax[4] = {0, 0, 0, 0};   // x-projection sums of the pending row
     double hs[4] = {0, 0, 0, 0};   // heat partial sums of the previous row
-    double ty[2 * NP];              // G* - dt Z_y of the current row
+    double ty[2 * NP_];              // G* - dt Z_y of the current row
 #pragma unroll
-    for (int q = 0; q < 2 * NP; ++q) ty[q] = 0.0;
+    for (int q = 0; q < 2 * NP_; ++q) ty[q] = 0.0;
 
     for (int j = j0s - 4; j <= j1s; ++j) {
         const int rx = j + 2;       // x-stage row
         const int rc = j + 1;       // recon row
         const bool row_j = j >= j0s && j < j1s;
-        // 0. tables for row j+3 (first used after this iteration's barriers);
-        //    stage the CellPar of row j+4 for the next iteration's builder
-        if (computes(j + 3))
-            build_tables(a, T3, *reinterpret_cast<const CellPar*>(pring + 32 * ((j + 3) & 3)),
-                         v1s, v2s, gauss);
+        // 0. stage the CellPar of row j+5 (its tables are built two
+        //    iterations from now)
         stage_par(j + 5, computes(j + 5));
         // 1. recon G*(j+1) = (G - dt Z) + dt Zhat_x
         if (computes(rc)) {
@@ -385,26 +414,26 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             const double b0 = fma(w2.x, a3, h2.x * a4), b1 = fma(w2.y, a3, h2.y * a4);
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                const double2 kw = lds2(T + koff_(p) + K_PE1);   // pE1, w1
-                const double h1 = T[koff_(p) + K_H1];
-                const double al = fma(kw.y, a2, fma(h1, a4, a1));
+            for (int p = 0; p < NP_; ++p) {
+                const double2 wh = lds2(T + koff_(p) + K_W1N);   // w1, h1
+                const double pe = T[koff_(p) + K_PE1];
+                const double al = fma(wh.x, a2, fma(wh.y, a4, a1));
                 const double2 t = lds2(R2 + off_(p));
-                sts2(R2 + off_(p), fma((al + b0) * kw.x, E2.x, t.x),
-                     fma((al + b1) * kw.x, E2.y, t.y));
+                sts2(R2 + off_(p), fma((al + b0) * pe, E2.x, t.x),
+                     fma((al + b1) * pe, E2.y, t.y));
             }
         } else if ((rc == j1s && k_hi != 0) || (rc == j0s - 1 && k_lo == 2)) {
             // ghost rows: zero (wall) or copy of the adjacent owned row
             const bool cp = rc == j1s && k_hi == 1;
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
+            for (int p = 0; p < NP_; ++p) {
                 const double2 s = cp ? lds2(R1 + off_(p)) : make_double2(0.0, 0.0);
                 sts2(R2 + off_(p), s.x, s.y);
             }
         }
         if (rc == j0s && k_lo == 1) {   // bottom ghost by copy, once G*(j0s) is complete
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
+            for (int p = 0; p < NP_; ++p) {
                 const double2 s = lds2(R2 + off_(p));
                 sts2(R1 + off_(p), s.x, s.y);
             }
@@ -418,11 +447,12 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
             const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             const double* gn = negy ? R2 : R0;
-            double c0[NP], c1[NP], c2[NP], c3[NP];
+            double c0[NP_], c1[NP_], c2[NP_], c3[NP_];
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                const double2 kw = lds2(T + koff_(p) + K_PE1);
-                const double h1 = T[koff_(p) + K_H1];
+            for (int p = 0; p < NP_; ++p) {
+                const double2 wh = lds2(T + koff_(p) + K_W1N);   // w1, h1
+                const double2 kw = make_double2(0.0, wh.x);
+                const double h1 = wh.y;
                 const double2 c = lds2(R1 + off_(p));
                 const double2 n = lds2(gn + off_(p));
                 const double y0 = cy0 * (c.x - n.x);
@@ -435,10 +465,10 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
                 c2[p] = fma(w2.x, y0, w2.y * y1);
                 c3[p] = fma(h1, ys, fma(h2.x, y0, h2.y * y1));
             }
-            s[0] = (c0[0] + c0[1]) + (c0[2] + c0[3]);
-            s[1] = (c1[0] + c1[1]) + (c1[2] + c1[3]);
-            s[2] = (c2[0] + c2[1]) + (c2[2] + c2[3]);
-            s[3] = (c3[0] + c3[1]) + (c3[2] + c3[3]);
+            s[0] = tsum<NP_>(c0);
+            s[1] = tsum<NP_>(c1);
+            s[2] = tsum<NP_>(c2);
+            s[3] = tsum<NP_>(c3);
         }
         // 3. x-stage of row j+2 into the slot of row j-1: G - dt Z_x
         const bool do_x = computes(rx);
@@ -447,12 +477,13 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
             const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             cp_async_wait_prev();   // this row's halos (staged one iteration ago)
-            double c0[NP], c1[NP], c2[NP], c3[NP];
+            double c0[NP_], c1[NP_], c2[NP_], c3[NP_];
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                const double2 kw = lds2(T + koff_(p) + K_PE1);
-                const double h1 = T[koff_(p) + K_H1];
-                const double2 c = pf[p], h = lds2(hst + 2 * (p * NT + tid));
+            for (int p = 0; p < NP_; ++p) {
+                const double2 wh = lds2(T + koff_(p) + K_W1N);   // w1, h1
+                const double2 kw = make_double2(0.0, wh.x);
+                const double h1 = wh.y;
+                const double2 c = pf[p], h = lds2(hst + 2 * (p * NT_ + tid));
                 const double y0 = cx[p] * (c.x - h.x), y1 = cx[p] * (c.y - h.y);
                 sts2(R0 + off_(p), c.x - y0, c.y - y1);
                 const double ys = y0 + y1;
@@ -461,19 +492,27 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
                 c2[p] = fma(w2.x, y0, w2.y * y1);
                 c3[p] = fma(h1, ys, fma(h2.x, y0, h2.y * y1));
             }
-            s[4] = (c0[0] + c0[1]) + (c0[2] + c0[3]);
-            s[5] = (c1[0] + c1[1]) + (c1[2] + c1[3]);
-            s[6] = (c2[0] + c2[1]) + (c2[2] + c2[3]);
-            s[7] = (c3[0] + c3[1]) + (c3[2] + c3[3]);
+            s[4] = tsum<NP_>(c0);
+            s[5] = tsum<NP_>(c1);
+            s[6] = tsum<NP_>(c2);
+            s[7] = tsum<NP_>(c3);
         }
         if (computes(rx + 1)) prefetch(rx + 1);
         s[8] = hs[0]; s[9] = hs[1]; s[10] = hs[2]; s[11] = hs[3];
         // 4. the row's block reduction; the CellPar staged one iteration
         //    ago (row j+4) lands before it
         cp_async_wait_prev();
-        reduce12(s, sred);
+        reduce12_begin<NT_>(s, sred);
+        // tables for row j+3, built while the reduction's second phase runs:
+        // slot T3 is read from iteration j+1 on, after this reduction's
+        // closing barrier, and every reader of its previous row has passed
+        // the opening barrier above
+        if (computes(j + 3))
+            build_tables<KS>(a, T3, *reinterpret_cast<const CellPar*>(pring + 32 * ((j + 3) & 3)),
+                             v1s, v2s, gauss);
+        reduce12_end<NT_>(s, sred);
         if (j - 1 >= j0s && j - 1 < j1s && tid < 4)
-            a.Hr[4 * ring_index(g, i, j - 1) + tid] = a.hfac * sred[12 * NT + 8 + tid];
+            a.Hr[4 * ring_index(g, i, j - 1) + tid] = a.hfac * sred[12 * NT_ + 8 + tid];
         if (do_x) {
             ax[0] = s[4]; ax[1] = s[5]; ax[2] = s[6]; ax[3] = s[7];
         }
@@ -506,12 +545,14 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
                 Xp = fexp(T[HD + H_GQ12] * T[KT + 8 * kb + K_W1] * W2.x);
             }
             double* out = out_b + (size_t)j * V_;
-            double e0[NP], e1[NP], e2[NP], e3[NP];
+            double e0[NP_], e1[NP_], e2[NP_], e3[NP_];
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
+            for (int p = 0; p < NP_; ++p) {
                 const double* K = T + koff_(p);
-                const double2 kw = lds2(K + K_PE1);     // pE1, w1
-                const double2 hW = lds2(K + K_H1);      // h1, W1
+                const double2 wh = lds2(K + K_W1N);     // w1, h1
+                const double2 pw = lds2(K + K_PE1);     // pE1, W1
+                const double2 kw = make_double2(pw.x, wh.x);
+                const double2 hW = make_double2(wh.y, pw.y);
                 const double al = fma(kw.y, a2, fma(hW.x, a4, a1));
                 const double M0 = kw.x * E2.x, M1 = kw.x * E2.y;
                 const double gs0 = fma(al + b0, M0, ty[2 * p]);
@@ -529,7 +570,7 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
                     acc1 = P1 * (M1 * mtw);
                     if (gauss) {
                         // (Gaussian - M)/eps (x wh), Gaussian = GA GB X
-                        const double2 gad = lds2(T + GK + 2 * (kb + 8 * p));   // GA', GD
+                        const double2 gad = lds2(T + GK + 2 * (kb + KS * p));   // GA', GD
                         acc0 = fma(gad.x * GB.x, Xp, fma(M0, -mew, acc0));
                         acc1 = fma(gad.x * GB.y, Xp * gad.y, fma(M1, -mew, acc1));
                     }
@@ -551,10 +592,10 @@ __global__ void __launch_bounds__(NT, 3) k_micro32(MicroArgs a) {
                 e3[p] = fma(t20, W2.x, t21 * W2.y);
                 Xp *= GR;
             }
-            hs[0] = (e0[0] + e0[1]) + (e0[2] + e0[3]);
-            hs[1] = (e1[0] + e1[1]) + (e1[2] + e1[3]);
-            hs[2] = (e2[0] + e2[1]) + (e2[2] + e2[3]);
-            hs[3] = (e3[0] + e3[1]) + (e3[2] + e3[3]);
+            hs[0] = tsum<NP_>(e0);
+            hs[1] = tsum<NP_>(e1);
+            hs[2] = tsum<NP_>(e2);
+            hs[3] = tsum<NP_>(e3);
         }
         // rotate slots for the next row
         {
