@@ -21,6 +21,9 @@ def __getattr__(name):
     if name in ("State2D", "step_2d", "run_2d", "Solver2D", "frame_moments", "get_solver"):
         from . import solver
         return getattr(solver, name)
+    if name in ("State1D", "step_1d", "run_1d", "Solver1D", "get_solver_1d"):
+        from . import solver1d
+        return getattr(solver1d, name)
     if name == "heat_flux_tensor_2d":
         from .macro2d import heat_flux_tensor_2d
         return heat_flux_tensor_2d
@@ -35,4 +38,5 @@ __all__ = ["Axis", "PhaseMesh", "TimePlan", "cell_centers", "plan_time", "PERIOD
            "BoundarySpec2D", "CollisionModel", "TempTensor2D", "conserved_1d",
            "conserved_2d", "primitives_1d", "primitives_2d", "ConfigurationError",
            "InvalidStateError", "NativeLibraryError", "State2D", "step_2d", "run_2d",
-           "Solver2D", "frame_moments", "heat_flux_tensor_2d", "run_parallel_2d"]
+           "Solver2D", "frame_moments", "heat_flux_tensor_2d", "run_parallel_2d",
+           "State1D", "step_1d", "run_1d", "Solver1D"]

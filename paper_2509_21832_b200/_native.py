@@ -19,9 +19,10 @@ LIB_PATH = PKG_DIR / "libmm2d.so"
 CSRC = PKG_DIR / "csrc"
 
 OK, ERR_CONFIG, ERR_STATE, ERR_INTERNAL = 0, 2, 3, 5
-STATE_DENSITY, STATE_PRESSURE, STATE_MODIFIED = 1, 2, 3
+STATE_DENSITY, STATE_PRESSURE, STATE_MODIFIED, STATE_TEMPERATURE = 1, 2, 3, 4
 STATE_MESSAGES = {
     STATE_DENSITY: "non-positive density",
+    STATE_TEMPERATURE: "non-positive temperature",
     STATE_PRESSURE: "pressure tensor is not positive definite",
     STATE_MODIFIED: "modified temperature tensor is not positive definite",
 }
@@ -47,6 +48,20 @@ class Config(C.Structure):
         ("nu", C.c_double),
         ("eps", C.c_double),
         ("px", C.c_int), ("py", C.c_int), ("rx", C.c_int), ("ry", C.c_int),
+        ("device", C.c_int),
+    ]
+
+
+class Config1D(C.Structure):
+    """mirror of struct mm1d_config (include/mm1d.h)"""
+    _fields_ = [
+        ("nx", C.c_int), ("x_min", C.c_double), ("x_max", C.c_double),
+        ("nv", C.c_int), ("v_min", C.c_double), ("v_max", C.c_double),
+        ("face", C.c_int * 2),
+        ("wall_T", C.c_double * 2),
+        ("tau_kind", C.c_int),
+        ("tau_value", C.c_double),
+        ("eps", C.c_double),
         ("device", C.c_int),
     ]
 
@@ -97,6 +112,16 @@ SIGNATURES = {
                                 [C.c_double, _vp, _vp]),
     "mm2d_time_kernels": (C.c_int, [_vp, C.c_double, C.c_int, _dp]),
     "mm2d_launch_count": (C.c_longlong, []),
+    "mm1d_create": (C.c_int, [C.POINTER(Config1D), C.POINTER(_vp)]),
+    "mm1d_destroy": (C.c_int, [_vp]),
+    "mm1d_last_error": (C.c_char_p, [_vp]),
+    "mm1d_step": (C.c_int, [_vp, _vp, _vp, C.c_double, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mm1d_upload": (C.c_int, [_vp, _vp, _vp]),
+    "mm1d_run": (C.c_int, [_vp, C.c_double, C.c_int]),
+    "mm1d_download": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "mm1d_resident": (C.c_int, [_vp]),
+    "mm1d_check": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                             C.POINTER(C.c_double)]),
     "mm2d_reset_launch_count": (None, []),
 }
 

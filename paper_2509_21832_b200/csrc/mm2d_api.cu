@@ -22,7 +22,8 @@
 
 using namespace mm2d;
 
-static std::atomic<long long> g_launches{0};
+// launches issued by this library (both the 2D and the 1D entry points)
+std::atomic<long long> g_launches{0};
 
 struct mm2d_ctx {
     mm2d_config cfg;

@@ -47,6 +47,33 @@ def problem_from_golden(name):
     return mesh, bc, p["eps"], model, p
 
 
+def problem1d_from_golden(name):
+    """1D (mesh, bc, eps, model, params) built with this repo's drop-in API."""
+    from paper_2509_21832_b200 import (Axis, BoundarySpec1D, CollisionModel, EXTRAPOLATE,
+                                       PERIODIC, PhaseMesh, WallSpec)
+    p = golden_index()[name]
+
+    def face(f):
+        if isinstance(f, dict):
+            return WallSpec(temperature=f["wall"])
+        return {"periodic": PERIODIC, "extrapolate": EXTRAPOLATE}[f]
+
+    mesh = PhaseMesh(space=(Axis(0.0, 1.0, p["nx"]),), velocity=(Axis(*p["v"]),))
+    bc = BoundarySpec1D(*(face(f) for f in p["faces"]))
+    model = CollisionModel(p["kind"])
+    return mesh, bc, p["eps"], model, p
+
+
+def q1_rel_err(Q, Qref):
+    """1D moments: max over (rho, rho u, E) of the rel L-inf error; momentum
+    is floored at max rho * sqrt(max T)."""
+    rho = Qref[:, 0]
+    T = 2.0 * Qref[:, 2] / rho - (Qref[:, 1] / rho) ** 2
+    s = [float(np.max(np.abs(Qref[:, c]))) for c in range(3)]
+    s[1] = max(s[1], float(np.max(rho)) * float(np.sqrt(np.max(T))))
+    return max(float(np.max(np.abs(Q[:, c] - Qref[:, c]))) / s[c] for c in range(3))
+
+
 def q_scales(Qref):
     """Per-component error scales for moment comparisons (SURVEY 8c floors:
     momentum uses max rho * sqrt(max T); E12 uses the diagonal maxima)."""

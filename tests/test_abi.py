@@ -9,9 +9,12 @@ from conftest import ROOT
 
 
 def header_symbols():
-    text = (ROOT / "include" / "mm2d.h").read_text()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(mm2d_\w+)\s*\(", text)))
+    syms = set()
+    for h in ("mm2d.h", "mm1d.h"):
+        text = (ROOT / "include" / h).read_text()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        syms |= set(re.findall(r"\b(mm[12]d_\w+)\s*\(", text))
+    return sorted(syms)
 
 
 def test_header_declares_the_boundary():
@@ -20,6 +23,8 @@ def test_header_declares_the_boundary():
                      "mm2d_k_transport_stage_2d", "mm2d_k_heat_tensor_2d"):
         assert required in syms
     assert len([s for s in syms if s.startswith("mm2d_k_")]) == 10
+    for required in ("mm1d_create", "mm1d_step", "mm1d_run", "mm1d_check"):
+        assert required in syms
 
 
 def test_library_exports_every_header_symbol():

@@ -182,3 +182,78 @@ def test_oracle_reproduces_reference_mms_pin(oracle):
     assert macro == pytest.approx(0.030605594996427687, rel=1e-12)
     assert micro == pytest.approx(0.031135911051471035, rel=1e-12)
     assert macro == pytest.approx(pin[0], rel=1e-12)
+
+
+# -- 1D manufactured solution (reference mms.py:1D part, restated) ----------
+# f = phi(v) psi(t,x), phi = e^{-(v-1)^2} + 2 e^{-(v+1)^2}, psi = 2 + sin 2pi(x-t);
+# exact macro (3 sqrt(pi) psi, -1/3, 25/18); g = (phi - 1.8 e^{-0.04(3v+1)^2}) psi / eps.
+
+MMS1_U, MMS1_T = -1.0 / 3.0, 25.0 / 18.0
+
+
+def mms1d_problem(n, eps=0.1):
+    from paper_2509_21832_b200 import (PERIODIC, Axis, BoundarySpec1D, CollisionModel,
+                                       PhaseMesh, cell_centers, conserved_1d)
+    mesh = PhaseMesh(space=(Axis(0.0, 1.0, n),), velocity=(Axis(-6.5, 6.5, n),))
+    bc = BoundarySpec1D(PERIODIC, PERIODIC)
+    model = CollisionModel("hard_sphere_1d")
+    x = cell_centers(mesh.space[0])
+    v = cell_centers(mesh.velocity[0])
+    tau = 3.2 * math.sqrt(MMS1_T / (2.0 * math.pi))
+    sp = math.sqrt(math.pi)
+
+    def psi(t, xx):
+        return 2.0 + np.sin(2.0 * np.pi * (xx - t))
+
+    def phi(vv):
+        return np.exp(-(vv - 1.0) ** 2) + 2.0 * np.exp(-(vv + 1.0) ** 2)
+
+    def g_exact(t, xx, vv):
+        shape = phi(vv) - 1.8 * np.exp(-0.04 * (3.0 * vv + 1.0) ** 2)
+        return psi(t, np.asarray(xx))[:, None] * shape[None, :] / eps
+
+    def h_perp(vv):
+        # h - Pi[h] for h = (v-1) phi at the exact state; moments (-4, 5.5, -7) sqrt(pi)
+        m0, m1, m2 = -4.0 * sp, 5.5 * sp, -7.0 * sp
+        u, T = MMS1_U, MMS1_T
+        w = (vv - u) / math.sqrt(T)
+        a1 = m0
+        a2 = (m1 - u * m0) / math.sqrt(T)
+        a3 = math.sqrt(2.0) * ((m2 - 2.0 * u * m1 + u * u * m0) / (2.0 * T) - 0.5 * m0)
+        unit = np.exp(-(vv - u) ** 2 / (2.0 * T)) / math.sqrt(2.0 * math.pi * T)
+        b3 = math.sqrt(2.0) * (0.5 * w * w - 0.5)
+        return (vv - 1.0) * phi(vv) - (a1 + w * a2 + b3 * a3) * unit
+
+    def micro_source(t, xx, vv):
+        c = 2.0 * np.pi * np.cos(2.0 * np.pi * (np.asarray(xx) - t))
+        return c[:, None] * h_perp(vv)[None, :] + tau * g_exact(t, xx, vv)
+
+    def macro_source(t, xx):
+        c = math.pi ** 1.5 * np.cos(2.0 * np.pi * (np.asarray(xx) - t))
+        return c[:, None] * np.array([-8.0, 11.0, -7.0])
+
+    def exact(t):
+        rho = 3.0 * sp * psi(t, x)
+        Q = conserved_1d(rho, np.full_like(rho, MMS1_U), np.full_like(rho, MMS1_T))
+        return Q, g_exact(t, x, v)
+
+    return mesh, bc, eps, model, exact, micro_source, macro_source
+
+
+def test_oracle_reproduces_reference_mms1d_pin(oracle):
+    """mms_run_1d(10): macro 0.06653393519741775, micro 0.09812773373649085
+    at rel 1e-12 (reference test_cases.py:98-102)."""
+    from paper_2509_21832_b200 import cell_centers, plan_time
+    mesh, bc, eps, model, exact, msrc, qsrc = mms1d_problem(10)
+    plan = plan_time(0.9351, 0.95, mesh)
+    prob = oracle.Problem1D(mesh, bc, eps, model)
+    x = cell_centers(mesh.space[0])
+    Q, G = exact(0.0)
+    for n in range(plan.n_steps):
+        t = n * plan.dt
+        Q, G, _ = oracle.step_1d_arrays(prob, Q, G, plan.dt, src=msrc(t, x, prob.v),
+                                        qsrc=qsrc(t, x))
+    Qe, Ge = exact(0.9351)
+    pin = golden_index()["mms"]["mms_run_1d_10"]
+    assert relative_l2(Q, Qe) == pytest.approx(pin[0], rel=1e-12)
+    assert relative_l2(G, Ge) == pytest.approx(pin[1], rel=1e-12)
