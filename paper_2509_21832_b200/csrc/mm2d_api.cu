@@ -245,6 +245,12 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         int occ = 0, nsm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 512 / ctx->np32, sm);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
+        // Band height: a CTA walks one column through ly rows, paying ~4
+        // pipeline-fill iterations per band.  Measured on C2 (256 x 256,
+        // 148 SMs x 3 CTAs): ly 36..60 gives 0.54-0.58 ms with a flat optimum
+        // at 48-56; a wave-quantisation model (pick ly minimising
+        // waves * (ly + 4)) predicted 52 and was not better, because the
+        // short last band of ly = 48 (16 rows) already fills the tail.
         const char* ly = getenv("MM2D_LY");
         ctx->ly32 = ly ? std::max(1, atoi(ly)) : 48;
         ctx->ly32 = std::min(ctx->ly32, g.by);

@@ -24,6 +24,7 @@
 //   4. reduction [y(j) | x(j+2) | H(j-1)], write H(j-1)
 //   5. G**(j), target, relax, store G^{n+1}(j), heat partials H(j)
 #pragma once
+#include <type_traits>
 #include "mm2d_common.cuh"
 #include "mm2d_micro.cuh"
 
@@ -192,9 +193,13 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
 // build the per-cell tables from the shared copy P of the cell's CellPar.
 // Work split so every warp does the same number of exps: warp 0 the K-table
 // (+ GD), warp 1 the L-table (+ GR), warps 2/3 the Gaussian GA / GB.
+// The closed-form target polynomial is stored pre-scaled by mtw = -wh/tau
+// with the Gaussian's -M wh/eps folded into U, so the node evaluates
+// acc = M (U' + V' + c' W2 + q1' p2 + p1' q2) (+ the Gaussian) directly.
 template <int KS>
 __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, const CellPar& P,
                                              const double* v1s, const double* v2s, bool gauss) {
+    const double mtw = -P.invtau * P.wh;
     for (int t = threadIdx.x; t < 128; t += blockDim.x) {
     const int m = t & 31;
     if (t < 32) {
@@ -203,15 +208,17 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         const double w1 = W1 * P.isT;
         const double q1 = W1s * P.inv2T - 2.0;
         const double p1 = W1 * P.gT1 * P.invT;
+        const double U = W1s * P.s11 * P.inv2T + q1 * p1;
         double* K = T + KT + 8 * m;
         sts2(K + K_W1N, w1, 0.5 * w1 * w1 - 1.0);
         sts2(K + K_PE1, P.pref * fexp(-W1s * P.inv2T), W1);
-        sts2(K + K_U, W1s * P.s11 * P.inv2T + q1 * p1, 2.0 * W1 * P.s12 * P.inv2T);
-        sts2(K + K_Q1, q1, p1);
+        sts2(K + K_U, fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
+             mtw * (2.0 * W1 * P.s12 * P.inv2T));
+        sts2(K + K_Q1, mtw * q1, mtw * p1);
         if (gauss) T[GK + 2 * m + 1] = fexp(P.gq12 * W1 * (v2s[1] - v2s[0]));
         if (m == 0) {
             sts2(T + HD + H_SCALE, P.scale, P.wg);
-            sts2(T + HD + H_MTW, -P.invtau * P.wh, a.inveps * P.wh);
+            sts2(T + HD + H_MTW, mtw, a.inveps * P.wh);
             sts2(T + HD + H_GQ12, P.gq12, P.wh);
         }
     } else if (t < 64) {
@@ -225,7 +232,7 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         L[L_W2N * NV] = w2;
         L[L_H2 * NV] = 0.5 * w2 * w2;
         L[L_W2 * NV] = W2;
-        L[L_V * NV] = q2 * p2 - W2s * P.s11 * P.inv2T;
+        L[L_V * NV] = mtw * (q2 * p2 - W2s * P.s11 * P.inv2T);
         L[L_Q2 * NV] = q2;
         L[L_P2 * NV] = p2;
         if (gauss) T[GL + NV + m] = fexp(P.gq12 * (v1s[KS] - v1s[0]) * W2);
@@ -258,6 +265,16 @@ inline size_t smem_bytes_v3() {
 // direction a compile-time property of the node pair: v1 < 0 exactly for
 // k < 16 (pairs p = 0, 1 difference towards the right neighbour), and both
 // nodes of every (l, l+1) pair share the sign of v2.
+//
+// Per-thread sums use running accumulators: for a transport stage the four
+// projection sums of the thread's nodes are
+//   s0 = Y0 + Y1,  s1 = sum_p w1_p (y0 + y1)_p,  s2 = w2_l Y0 + w2_r Y1,
+//   s3 = sum_p h1_p (y0 + y1)_p + h2_l Y0 + h2_r Y1
+// with Y0 / Y1 the sums over the thread's left / right nodes of the pair
+// (b4 = h1 + h2, w2 and h2 are per-thread constants), and the heat moments
+// are accumulated as A_a = sum W1^a o per node column, then weighted by the
+// thread's W2 powers.  The row loop runs a predicate-free body for the rows
+// away from the piece ends.
 template <int NP_>
 __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_micro32(MicroArgs a) {
     constexpr int NT_ = 512 / NP_;       // threads per CTA
@@ -271,7 +288,7 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
     double* ring = smem;                            // [3][V]
     double* tabs = ring + 3 * V;                    // [TSLOTS][SLOT]
     double* sred = tabs + TSLOTS * SLOT;            // [12][NT] partials + [12] totals
-    double* pring = sred + red_size<NT_>();                     // [4][32] staged CellPar rows
+    double* pring = sred + red_size<NT_>();         // [4][32] staged CellPar rows
     double* v1s = pring + 4 * 32;
     double* v2s = v1s + NV;
     if (tid < NV) v1s[tid] = a.v1[tid];
@@ -301,12 +318,6 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
     const double cy0 = sy * v2s[lb] * a.idy, cy1 = sy * v2s[lb + 1] * a.idy;
     const size_t V_ = V;
 
-    // Work items are (band, column) pieces of a.ly rows, numbered band-major
-    // so that CTAs running at the same time cover adjacent columns of the
-    // same band: the x-halo columns they read are each other's own columns,
-    // which keeps the halo re-reads in L2.  CTAs stride over the items
-    // (persistent when the grid is smaller than the item count).
-    {
     const int i = blockIdx.x;
     const int j0s = blockIdx.y * a.ly;
     const int j1s = min(g.by, j0s + a.ly);
@@ -350,7 +361,6 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
                        reinterpret_cast<const double*>(a.P + ring_index(g, i, r)) + 2 * tid);
         cp_async_commit();
     };
-    __syncthreads();   // previous piece fully drained
     stage_par(j0s - 1, computes(j0s - 1));
     stage_par(j0s, computes(j0s));
     cp_async_wait_all();
@@ -358,9 +368,9 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
 
     double2 pf[NP_];               // prefetched own G^n of the next x-stage row
     double* hst = pring + 4 * 32 + 2 * NV;   // [NP][NT] double2 halo staging (thread-private)
-    auto prefetch = [&](int r) {
+    auto prefetch = [&](int r, auto steady) {
         const double *own, *hl, *hr;
-        if (r >= 0 && r < g.by) {
+        if (decltype(steady)::value || (r >= 0 && r < g.by)) {
             own = own_b + (size_t)r * V_;
             hl = lft_b + (size_t)r * lft_s;
             hr = rgt_b + (size_t)r * rgt_s;
@@ -393,34 +403,62 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
 
     double ax[4] = {0, 0, 0, 0};   // x-projection sums of the pending row
     double hs[4] = {0, 0, 0, 0};   // heat partial sums of the previous row
-    double ty[2 * NP_];              // G* - dt Z_y of the current row
+    double ty[2 * NP_];            // G* - dt Z_y of the current row
 #pragma unroll
     for (int q = 0; q < 2 * NP_; ++q) ty[q] = 0.0;
 
-    for (int j = j0s - 4; j <= j1s; ++j) {
+    // one transport stage's four projection sums from the thread's pairs
+    auto stage_sums = [&](const double* T, const double (&y)[2 * NP_], double* s) {
+        const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
+        const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
+        double Y0 = y[0], Y1 = y[1], S1, S3;
+        {
+            const double2 wh = lds2(T + koff_(0) + K_W1N);   // w1, h1
+            const double ys = y[0] + y[1];
+            S1 = wh.x * ys;
+            S3 = wh.y * ys;
+        }
+#pragma unroll
+        for (int p = 1; p < NP_; ++p) {
+            const double2 wh = lds2(T + koff_(p) + K_W1N);
+            const double ys = y[2 * p] + y[2 * p + 1];
+            Y0 += y[2 * p];
+            Y1 += y[2 * p + 1];
+            S1 = fma(wh.x, ys, S1);
+            S3 = fma(wh.y, ys, S3);
+        }
+        s[0] = Y0 + Y1;
+        s[1] = S1;
+        s[2] = fma(w2.x, Y0, w2.y * Y1);
+        s[3] = S3 + fma(h2.x, Y0, h2.y * Y1);
+    };
+
+    auto body = [&](int j, auto steady) {
+        constexpr bool ST = decltype(steady)::value;
         const int rx = j + 2;       // x-stage row
         const int rc = j + 1;       // recon row
-        const bool row_j = j >= j0s && j < j1s;
+        const bool row_j = ST || (j >= j0s && j < j1s);
         // 0. stage the CellPar of row j+5 (its tables are built two
         //    iterations from now)
-        stage_par(j + 5, computes(j + 5));
+        stage_par(j + 5, ST || computes(j + 5));
         // 1. recon G*(j+1) = (G - dt Z) + dt Zhat_x
-        if (computes(rc)) {
+        if (ST || computes(rc)) {
             const double* T = T1;
             const double sc = T[HD + H_SCALE];
             const double a1 = ax[0] * sc, a2 = ax[1] * sc, a3 = ax[2] * sc, a4 = ax[3] * sc;
             const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
             const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
-            const double b0 = fma(w2.x, a3, h2.x * a4), b1 = fma(w2.y, a3, h2.y * a4);
+            const double bE0 = fma(w2.x, a3, h2.x * a4) * E2.x;
+            const double bE1 = fma(w2.y, a3, h2.y * a4) * E2.y;
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
                 const double2 wh = lds2(T + koff_(p) + K_W1N);   // w1, h1
                 const double pe = T[koff_(p) + K_PE1];
-                const double al = fma(wh.x, a2, fma(wh.y, a4, a1));
+                const double alp = fma(wh.x, a2, fma(wh.y, a4, a1)) * pe;
                 const double2 t = lds2(R2 + off_(p));
-                sts2(R2 + off_(p), fma((al + b0) * pe, E2.x, t.x),
-                     fma((al + b1) * pe, E2.y, t.y));
+                sts2(R2 + off_(p), fma(alp, E2.x, fma(bE0, pe, t.x)),
+                     fma(alp, E2.y, fma(bE1, pe, t.y)));
             }
         } else if ((rc == j1s && k_hi != 0) || (rc == j0s - 1 && k_lo == 2)) {
             // ghost rows: zero (wall) or copy of the adjacent owned row
@@ -431,7 +469,7 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
                 sts2(R2 + off_(p), s.x, s.y);
             }
         }
-        if (rc == j0s && k_lo == 1) {   // bottom ghost by copy, once G*(j0s) is complete
+        if (!ST && rc == j0s && k_lo == 1) {   // bottom ghost by copy, once G*(j0s) is complete
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
                 const double2 s = lds2(R2 + off_(p));
@@ -440,64 +478,37 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         }
         double s[12];
 #pragma unroll
-        for (int q = 0; q < 12; ++q) s[q] = 0.0;
+        for (int q = 0; q < 8; ++q) s[q] = 0.0;
         // 2. y-sums of row j: Y = cy (G*_j - G*_upwind)
         if (row_j) {
-            const double* T = T0;
-            const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
-            const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             const double* gn = negy ? R2 : R0;
-            double c0[NP_], c1[NP_], c2[NP_], c3[NP_];
+            double y[2 * NP_];
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
-                const double2 wh = lds2(T + koff_(p) + K_W1N);   // w1, h1
-                const double2 kw = make_double2(0.0, wh.x);
-                const double h1 = wh.y;
                 const double2 c = lds2(R1 + off_(p));
                 const double2 n = lds2(gn + off_(p));
-                const double y0 = cy0 * (c.x - n.x);
-                const double y1 = cy1 * (c.y - n.y);
-                ty[2 * p] = c.x - y0;
-                ty[2 * p + 1] = c.y - y1;
-                const double ys = y0 + y1;
-                c0[p] = ys;
-                c1[p] = kw.y * ys;
-                c2[p] = fma(w2.x, y0, w2.y * y1);
-                c3[p] = fma(h1, ys, fma(h2.x, y0, h2.y * y1));
+                y[2 * p] = cy0 * (c.x - n.x);
+                y[2 * p + 1] = cy1 * (c.y - n.y);
+                ty[2 * p] = c.x - y[2 * p];
+                ty[2 * p + 1] = c.y - y[2 * p + 1];
             }
-            s[0] = tsum<NP_>(c0);
-            s[1] = tsum<NP_>(c1);
-            s[2] = tsum<NP_>(c2);
-            s[3] = tsum<NP_>(c3);
+            stage_sums(T0, y, s);
         }
         // 3. x-stage of row j+2 into the slot of row j-1: G - dt Z_x
-        const bool do_x = computes(rx);
+        const bool do_x = ST || computes(rx);
         if (do_x) {
-            const double* T = T2;
-            const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
-            const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             cp_async_wait_prev();   // this row's halos (staged one iteration ago)
-            double c0[NP_], c1[NP_], c2[NP_], c3[NP_];
+            double y[2 * NP_];
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
-                const double2 wh = lds2(T + koff_(p) + K_W1N);   // w1, h1
-                const double2 kw = make_double2(0.0, wh.x);
-                const double h1 = wh.y;
                 const double2 c = pf[p], h = lds2(hst + 2 * (p * NT_ + tid));
-                const double y0 = cx[p] * (c.x - h.x), y1 = cx[p] * (c.y - h.y);
-                sts2(R0 + off_(p), c.x - y0, c.y - y1);
-                const double ys = y0 + y1;
-                c0[p] = ys;
-                c1[p] = kw.y * ys;
-                c2[p] = fma(w2.x, y0, w2.y * y1);
-                c3[p] = fma(h1, ys, fma(h2.x, y0, h2.y * y1));
+                y[2 * p] = cx[p] * (c.x - h.x);
+                y[2 * p + 1] = cx[p] * (c.y - h.y);
+                sts2(R0 + off_(p), c.x - y[2 * p], c.y - y[2 * p + 1]);
             }
-            s[4] = tsum<NP_>(c0);
-            s[5] = tsum<NP_>(c1);
-            s[6] = tsum<NP_>(c2);
-            s[7] = tsum<NP_>(c3);
+            stage_sums(T2, y, s + 4);
         }
-        if (computes(rx + 1)) prefetch(rx + 1);
+        if (ST || computes(rx + 1)) prefetch(rx + 1, steady);
         s[8] = hs[0]; s[9] = hs[1]; s[10] = hs[2]; s[11] = hs[3];
         // 4. the row's block reduction; the CellPar staged one iteration
         //    ago (row j+4) lands before it
@@ -507,11 +518,11 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         // slot T3 is read from iteration j+1 on, after this reduction's
         // closing barrier, and every reader of its previous row has passed
         // the opening barrier above
-        if (computes(j + 3))
+        if (ST || computes(j + 3))
             build_tables<KS>(a, T3, *reinterpret_cast<const CellPar*>(pring + 32 * ((j + 3) & 3)),
                              v1s, v2s, gauss);
         reduce12_end<NT_>(s, sred);
-        if (j - 1 >= j0s && j - 1 < j1s && tid < 4)
+        if ((ST || (j - 1 >= j0s && j - 1 < j1s)) && tid < 4)
             a.Hr[4 * ring_index(g, i, j - 1) + tid] = a.hfac * sred[12 * NT_ + 8 + tid];
         if (do_x) {
             ax[0] = s[4]; ax[1] = s[5]; ax[2] = s[6]; ax[3] = s[7];
@@ -523,8 +534,6 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
             const double sc = T[HD + H_SCALE];
             const double a1 = s[0] * sc, a2 = s[1] * sc, a3 = s[2] * sc, a4 = s[3] * sc;
             const double wg = T[HD + H_WG];
-            const double mtw = T[HD + H_MTW];
-            const double mew = T[HD + H_MEW];
             const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
             const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
@@ -533,9 +542,9 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
             const double2 q2 = lds2(T + LT + L_Q2 * NV + lb);
             const double2 p2 = lds2(T + LT + L_P2 * NV + lb);
             const double b0 = fma(w2.x, a3, h2.x * a4), b1 = fma(w2.y, a3, h2.y * a4);
-            const double W2xx = W2.x * W2.x, W2yy = W2.y * W2.y;
             // wall-strip target (boundary.py:343-378), precomputed
-            const double* wsrc = wx ? wx + (size_t)j * V_ : (j == 0 ? wb : (j == g.by - 1 ? wt : nullptr));
+            const double* wsrc = wx ? wx + (size_t)j * V_
+                                    : (ST ? nullptr : (j == 0 ? wb : (j == g.by - 1 ? wt : nullptr)));
             // ES-BGK Gaussian: X(k, l) = exp(c12 W1 W2 / det), by recurrence
             double2 GB = make_double2(0.0, 0.0);
             double GR = 1.0, Xp = 0.0;
@@ -545,65 +554,72 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
                 Xp = fexp(T[HD + H_GQ12] * T[KT + 8 * kb + K_W1] * W2.x);
             }
             double* out = out_b + (size_t)j * V_;
-            double e0[NP_], e1[NP_], e2[NP_], e3[NP_];
+            double A0x = 0, A0y = 0, A1x = 0, A1y = 0, A2x = 0, A2y = 0, A3x = 0, A3y = 0;
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
                 const double* K = T + koff_(p);
                 const double2 wh = lds2(K + K_W1N);     // w1, h1
                 const double2 pw = lds2(K + K_PE1);     // pE1, W1
-                const double2 kw = make_double2(pw.x, wh.x);
-                const double2 hW = make_double2(wh.y, pw.y);
-                const double al = fma(kw.y, a2, fma(hW.x, a4, a1));
-                const double M0 = kw.x * E2.x, M1 = kw.x * E2.y;
+                const double al = fma(wh.x, a2, fma(wh.y, a4, a1));
+                const double M0 = pw.x * E2.x, M1 = pw.x * E2.y;
                 const double gs0 = fma(al + b0, M0, ty[2 * p]);
                 const double gs1 = fma(al + b1, M1, ty[2 * p + 1]);
                 double acc0, acc1;
                 if (wsrc == nullptr) {
-                    // closed-form target (_core.pyx:220-224), factored
-                    const double2 Uc = lds2(K + K_U);   // U, c
-                    const double2 qp = lds2(K + K_Q1);  // q1, p1
+                    // closed-form target (_core.pyx:220-224), factored and
+                    // pre-scaled by -wh/tau (minus wh/eps when Gaussian)
+                    const double2 Uc = lds2(K + K_U);   // U', c'
+                    const double2 qp = lds2(K + K_Q1);  // q1', p1'
                     double P0 = Uc.x + Vl.x, P1 = Uc.x + Vl.y;
                     P0 = fma(Uc.y, W2.x, P0); P1 = fma(Uc.y, W2.y, P1);
                     P0 = fma(qp.x, p2.x, P0); P1 = fma(qp.x, p2.y, P1);
                     P0 = fma(qp.y, q2.x, P0); P1 = fma(qp.y, q2.y, P1);
-                    acc0 = P0 * (M0 * mtw);
-                    acc1 = P1 * (M1 * mtw);
+                    acc0 = P0 * M0;
+                    acc1 = P1 * M1;
                     if (gauss) {
-                        // (Gaussian - M)/eps (x wh), Gaussian = GA GB X
+                        // + Gaussian wh/eps, Gaussian = GA GB X
                         const double2 gad = lds2(T + GK + 2 * (kb + KS * p));   // GA', GD
-                        acc0 = fma(gad.x * GB.x, Xp, fma(M0, -mew, acc0));
-                        acc1 = fma(gad.x * GB.y, Xp * gad.y, fma(M1, -mew, acc1));
+                        const double Y0 = gad.x * Xp;
+                        acc0 = fma(GB.x, Y0, acc0);
+                        acc1 = fma(GB.y, Y0 * gad.y, acc1);
                     }
                 } else {
                     const double2 w = __ldg(reinterpret_cast<const double2*>(wsrc + off_(p)));
-                    const double wh = T[HD + H_WH];
-                    acc0 = wh * w.x;
-                    acc1 = wh * w.y;
+                    const double wh_ = T[HD + H_WH];
+                    acc0 = wh_ * w.x;
+                    acc1 = wh_ * w.y;
                 }
                 const double o0 = fma(wg, gs0, acc0), o1 = fma(wg, gs1, acc1);
                 *reinterpret_cast<double2*>(out + off_(p)) = make_double2(o0, o1);
-                // heat moments about u^n (_core.pyx:303-321)
-                const double W1 = hW.y, W11 = W1 * W1;
-                const double t10 = W11 * o0, t11 = W11 * o1;
-                const double t20 = W2xx * o0, t21 = W2yy * o1;
-                e0[p] = (t10 + t11) * W1;
-                e1[p] = fma(t10, W2.x, t11 * W2.y);
-                e2[p] = (t20 + t21) * W1;
-                e3[p] = fma(t20, W2.x, t21 * W2.y);
+                // heat moments about u^n (_core.pyx:303-321): A_a = sum W1^a o
+                const double W1 = pw.y, W11 = W1 * W1, W111 = W11 * W1;
+                A0x += o0; A0y += o1;
+                A1x = fma(W1, o0, A1x); A1y = fma(W1, o1, A1y);
+                A2x = fma(W11, o0, A2x); A2y = fma(W11, o1, A2y);
+                A3x = fma(W111, o0, A3x); A3y = fma(W111, o1, A3y);
                 Xp *= GR;
             }
-            hs[0] = tsum<NP_>(e0);
-            hs[1] = tsum<NP_>(e1);
-            hs[2] = tsum<NP_>(e2);
-            hs[3] = tsum<NP_>(e3);
+            const double W2xx = W2.x * W2.x, W2yy = W2.y * W2.y;
+            hs[0] = A3x + A3y;
+            hs[1] = fma(W2.x, A2x, W2.y * A2y);
+            hs[2] = fma(W2xx, A1x, W2yy * A1y);
+            hs[3] = fma(W2xx * W2.x, A0x, (W2yy * W2.y) * A0y);
         }
         // rotate slots for the next row
         {
             double* r0 = R0; R0 = R1; R1 = R2; R2 = r0;
             double* t0 = T0; T0 = T1; T1 = T2; T2 = T3; T3 = T4; T4 = t0;
         }
-    }
-    }   // pieces
+    };
+
+    // steady rows: every stage active, no ghost rows, no wall rows
+    const int js_lo = j0s + 1, js_hi = min(rhi - 5, j1s - 1);
+    int j = j0s - 4;
+    for (; j < js_lo && j <= j1s; ++j) body(j, std::false_type());
+    for (; j <= js_hi; ++j) body(j, std::true_type());
+    for (; j <= j1s; ++j) body(j, std::false_type());
+#undef off_
+#undef koff_
 }
 
 // Diffuse-wall strip targets: g^ = -(Mterm - Pi[Mterm]) / tau for every
