@@ -35,7 +35,8 @@ constexpr int NV = 32;
 constexpr int V = NV * NV;
 constexpr int NT = 128;              // threads of the default 8-node (NP = 4) variant
 constexpr int NP = 4;                // node pairs per thread (default variant)
-constexpr int TSLOTS = 5;            // table slots (rows j..j+3 + WAR margin)
+constexpr int TSLOTS = 4;            // table slots (rows j..j+3; the slot rebuilt
+                                     // at iteration j last held row j-1)
 constexpr int KT = 0;                // K-table [32][8]
 constexpr int LT = KT + 8 * NV;      // L-table [8][32]
 constexpr int GK = LT + 8 * NV;      // Gaussian k-table [32][2] (GA, GD)
@@ -255,10 +256,39 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
+// Bulk (TMA) copies global -> shared completing on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "MBW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra MBW_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 template <int NP_>
 inline size_t smem_bytes_v3() {
     constexpr int NT_ = 512 / NP_;
-    return sizeof(double) * (3 * V + TSLOTS * SLOT + red_size<NT_>() + 4 * 32 + 2 * NV + 2 * NP_ * NT_);
+    return sizeof(double) * (3 * V + 2 * V + TSLOTS * SLOT + red_size<NT_>() + 4 * 32 + 2 * NV + 2);
 }
 
 // The host selects this kernel only when the velocity axes make the upwind
@@ -286,7 +316,8 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
     const int kb = tid >> 4, lb = (tid & 15) << 1;
 
     double* ring = smem;                            // [3][V]
-    double* tabs = ring + 3 * V;                    // [TSLOTS][SLOT]
+    double* stg = ring + 3 * V;                     // [2][V] x-stage row: own | halo
+    double* tabs = stg + 2 * V;                     // [TSLOTS][SLOT]
     double* sred = tabs + TSLOTS * SLOT;            // [12][NT] partials + [12] totals
     double* pring = sred + red_size<NT_>();         // [4][32] staged CellPar rows
     double* v1s = pring + 4 * 32;
@@ -366,9 +397,20 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
     cp_async_wait_all();
     __syncthreads();
 
-    double2 pf[NP_];               // prefetched own G^n of the next x-stage row
-    double* hst = pring + 4 * 32 + 2 * NV;   // [NP][NT] double2 halo staging (thread-private)
+    // x-stage rows arrive by TMA: own row -> stg[0:V], the right neighbour's
+    // k < 16 half -> stg[V:V+V/2], the left neighbour's k >= 16 half ->
+    // stg[V+V/2:2V], so every node's upwind neighbour sits at the node's own
+    // offset.  Thread 0 arms the mbarrier and issues three bulk copies once
+    // the previous row's readers have passed a CTA barrier.
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(v2s + NV);
+    if (tid == 0) {
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    unsigned nload = 0;            // bulk loads issued (mbarrier phase = parity)
     auto prefetch = [&](int r, auto steady) {
+        if (tid != 0) { ++nload; return; }
         const double *own, *hl, *hr;
         if (decltype(steady)::value || (r >= 0 && r < g.by)) {
             own = own_b + (size_t)r * V_;
@@ -382,12 +424,12 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
             if (!hl) hl = a.zero;
             if (!hr) hr = a.zero;
         }
-#pragma unroll
-        for (int p = 0; p < NP_; ++p) {
-            pf[p] = __ldg(reinterpret_cast<const double2*>(own + off_(p)));
-            cp_async16(hst + 2 * (p * NT_ + tid), (p < NP_ / 2 ? hr : hl) + off_(p));
-        }
-        cp_async_commit();
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(mbar, 2 * V * sizeof(double));
+        bulk_g2s(stg, own, V * sizeof(double), mbar);
+        bulk_g2s(stg + V, hr, V / 2 * sizeof(double), mbar);
+        bulk_g2s(stg + V + V / 2, hl + V / 2, V / 2 * sizeof(double), mbar);
+        ++nload;
     };
 
     // rotating slot pointers: ring rows (j-1, j, j+1); table rows
@@ -399,7 +441,6 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
     double* T1 = tabs + SLOT;
     double* T2 = tabs + 2 * SLOT;
     double* T3 = tabs + 3 * SLOT;
-    double* T4 = tabs + 4 * SLOT;
 
     double ax[4] = {0, 0, 0, 0};   // x-projection sums of the pending row
     double hs[4] = {0, 0, 0, 0};   // heat partial sums of the previous row
@@ -497,23 +538,24 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         // 3. x-stage of row j+2 into the slot of row j-1: G - dt Z_x
         const bool do_x = ST || computes(rx);
         if (do_x) {
-            cp_async_wait_prev();   // this row's halos (staged one iteration ago)
+            mbar_wait(mbar, (nload - 1) & 1);   // this row's bulk loads (issued one iteration ago)
             double y[2 * NP_];
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
-                const double2 c = pf[p], h = lds2(hst + 2 * (p * NT_ + tid));
+                const double2 c = lds2(stg + off_(p)), h = lds2(stg + V + off_(p));
                 y[2 * p] = cx[p] * (c.x - h.x);
                 y[2 * p + 1] = cx[p] * (c.y - h.y);
                 sts2(R0 + off_(p), c.x - y[2 * p], c.y - y[2 * p + 1]);
             }
             stage_sums(T2, y, s + 4);
         }
-        if (ST || computes(rx + 1)) prefetch(rx + 1, steady);
         s[8] = hs[0]; s[9] = hs[1]; s[10] = hs[2]; s[11] = hs[3];
         // 4. the row's block reduction; the CellPar staged one iteration
         //    ago (row j+4) lands before it
         cp_async_wait_prev();
         reduce12_begin<NT_>(s, sred);
+        // every thread is past this row's x-stage reads: refill the staging
+        if (ST || computes(rx + 1)) prefetch(rx + 1, steady);
         // tables for row j+3, built while the reduction's second phase runs:
         // slot T3 is read from iteration j+1 on, after this reduction's
         // closing barrier, and every reader of its previous row has passed
@@ -608,7 +650,7 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         // rotate slots for the next row
         {
             double* r0 = R0; R0 = R1; R1 = R2; R2 = r0;
-            double* t0 = T0; T0 = T1; T1 = T2; T2 = T3; T3 = T4; T4 = t0;
+            double* t0 = T0; T0 = T1; T1 = T2; T2 = T3; T3 = t0;
         }
     };
 
