@@ -563,13 +563,68 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         if (ST || computes(j + 3))
             build_tables<KS>(a, T3, *reinterpret_cast<const CellPar*>(pring + 32 * ((j + 3) & 3)),
                              v1s, v2s, gauss);
+        // target + Gaussian of row j: independent of the projection sums, so
+        // it is evaluated inside the reduction window
+        double acc[2 * NP_];
+        const double* wsrc = wx ? wx + (size_t)j * V_
+                                : (ST ? nullptr : (j == 0 ? wb : (j == g.by - 1 ? wt : nullptr)));
+        if (row_j) {
+            const double* T = T0;
+            const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
+            const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
+            if (wsrc == nullptr) {
+                const double2 Vl = lds2(T + LT + L_V * NV + lb);
+                const double2 q2 = lds2(T + LT + L_Q2 * NV + lb);
+                const double2 p2 = lds2(T + LT + L_P2 * NV + lb);
+                // ES-BGK Gaussian: X(k, l) = exp(c12 W1 W2 / det), by recurrence
+                double2 GB = make_double2(0.0, 0.0);
+                double GR = 1.0, Xp = 0.0;
+                if (gauss) {
+                    GB = lds2(T + GL + lb);
+                    GR = T[GL + NV + lb];
+                    Xp = fexp(T[HD + H_GQ12] * T[KT + 8 * kb + K_W1] * W2.x);
+                }
+#pragma unroll
+                for (int p = 0; p < NP_; ++p) {
+                    const double* K = T + koff_(p);
+                    const double pe = K[K_PE1];
+                    // closed-form target (_core.pyx:220-224), factored and
+                    // pre-scaled by -wh/tau (minus wh/eps when Gaussian)
+                    const double2 Uc = lds2(K + K_U);   // U', c'
+                    const double2 qp = lds2(K + K_Q1);  // q1', p1'
+                    double P0 = Uc.x + Vl.x, P1 = Uc.x + Vl.y;
+                    P0 = fma(Uc.y, W2.x, P0); P1 = fma(Uc.y, W2.y, P1);
+                    P0 = fma(qp.x, p2.x, P0); P1 = fma(qp.x, p2.y, P1);
+                    P0 = fma(qp.y, q2.x, P0); P1 = fma(qp.y, q2.y, P1);
+                    acc[2 * p] = P0 * (pe * E2.x);
+                    acc[2 * p + 1] = P1 * (pe * E2.y);
+                    if (gauss) {
+                        // + Gaussian wh/eps, Gaussian = GA GB X
+                        const double2 gad = lds2(T + GK + 2 * (kb + KS * p));   // GA', GD
+                        const double Y0 = gad.x * Xp;
+                        acc[2 * p] = fma(GB.x, Y0, acc[2 * p]);
+                        acc[2 * p + 1] = fma(GB.y, Y0 * gad.y, acc[2 * p + 1]);
+                        Xp *= GR;
+                    }
+                }
+            } else {
+                // wall-strip target (boundary.py:343-378), precomputed
+                const double wh_ = T[HD + H_WH];
+#pragma unroll
+                for (int p = 0; p < NP_; ++p) {
+                    const double2 w = __ldg(reinterpret_cast<const double2*>(wsrc + off_(p)));
+                    acc[2 * p] = wh_ * w.x;
+                    acc[2 * p + 1] = wh_ * w.y;
+                }
+            }
+        }
         reduce12_end<NT_>(s, sred);
         if ((ST || (j - 1 >= j0s && j - 1 < j1s)) && tid < 4)
             a.Hr[4 * ring_index(g, i, j - 1) + tid] = a.hfac * sred[12 * NT_ + 8 + tid];
         if (do_x) {
             ax[0] = s[4]; ax[1] = s[5]; ax[2] = s[6]; ax[3] = s[7];
         }
-        // 5. G**(j), target, relax, store, heat partials
+        // 5. G**(j), relax, store, heat partials
         hs[0] = hs[1] = hs[2] = hs[3] = 0.0;
         if (row_j) {
             const double* T = T0;
@@ -580,21 +635,7 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
             const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
-            const double2 Vl = lds2(T + LT + L_V * NV + lb);
-            const double2 q2 = lds2(T + LT + L_Q2 * NV + lb);
-            const double2 p2 = lds2(T + LT + L_P2 * NV + lb);
             const double b0 = fma(w2.x, a3, h2.x * a4), b1 = fma(w2.y, a3, h2.y * a4);
-            // wall-strip target (boundary.py:343-378), precomputed
-            const double* wsrc = wx ? wx + (size_t)j * V_
-                                    : (ST ? nullptr : (j == 0 ? wb : (j == g.by - 1 ? wt : nullptr)));
-            // ES-BGK Gaussian: X(k, l) = exp(c12 W1 W2 / det), by recurrence
-            double2 GB = make_double2(0.0, 0.0);
-            double GR = 1.0, Xp = 0.0;
-            if (gauss) {
-                GB = lds2(T + GL + lb);
-                GR = T[GL + NV + lb];
-                Xp = fexp(T[HD + H_GQ12] * T[KT + 8 * kb + K_W1] * W2.x);
-            }
             double* out = out_b + (size_t)j * V_;
             double A0x = 0, A0y = 0, A1x = 0, A1y = 0, A2x = 0, A2y = 0, A3x = 0, A3y = 0;
 #pragma unroll
@@ -606,32 +647,7 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
                 const double M0 = pw.x * E2.x, M1 = pw.x * E2.y;
                 const double gs0 = fma(al + b0, M0, ty[2 * p]);
                 const double gs1 = fma(al + b1, M1, ty[2 * p + 1]);
-                double acc0, acc1;
-                if (wsrc == nullptr) {
-                    // closed-form target (_core.pyx:220-224), factored and
-                    // pre-scaled by -wh/tau (minus wh/eps when Gaussian)
-                    const double2 Uc = lds2(K + K_U);   // U', c'
-                    const double2 qp = lds2(K + K_Q1);  // q1', p1'
-                    double P0 = Uc.x + Vl.x, P1 = Uc.x + Vl.y;
-                    P0 = fma(Uc.y, W2.x, P0); P1 = fma(Uc.y, W2.y, P1);
-                    P0 = fma(qp.x, p2.x, P0); P1 = fma(qp.x, p2.y, P1);
-                    P0 = fma(qp.y, q2.x, P0); P1 = fma(qp.y, q2.y, P1);
-                    acc0 = P0 * M0;
-                    acc1 = P1 * M1;
-                    if (gauss) {
-                        // + Gaussian wh/eps, Gaussian = GA GB X
-                        const double2 gad = lds2(T + GK + 2 * (kb + KS * p));   // GA', GD
-                        const double Y0 = gad.x * Xp;
-                        acc0 = fma(GB.x, Y0, acc0);
-                        acc1 = fma(GB.y, Y0 * gad.y, acc1);
-                    }
-                } else {
-                    const double2 w = __ldg(reinterpret_cast<const double2*>(wsrc + off_(p)));
-                    const double wh_ = T[HD + H_WH];
-                    acc0 = wh_ * w.x;
-                    acc1 = wh_ * w.y;
-                }
-                const double o0 = fma(wg, gs0, acc0), o1 = fma(wg, gs1, acc1);
+                const double o0 = fma(wg, gs0, acc[2 * p]), o1 = fma(wg, gs1, acc[2 * p + 1]);
                 *reinterpret_cast<double2*>(out + off_(p)) = make_double2(o0, o1);
                 // heat moments about u^n (_core.pyx:303-321): A_a = sum W1^a o
                 const double W1 = pw.y, W11 = W1 * W1, W111 = W11 * W1;
@@ -639,7 +655,6 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
                 A1x = fma(W1, o0, A1x); A1y = fma(W1, o1, A1y);
                 A2x = fma(W11, o0, A2x); A2y = fma(W11, o1, A2y);
                 A3x = fma(W111, o0, A3x); A3y = fma(W111, o1, A3y);
-                Xp *= GR;
             }
             const double W2xx = W2.x * W2.x, W2yy = W2.y * W2.y;
             hs[0] = A3x + A3y;
