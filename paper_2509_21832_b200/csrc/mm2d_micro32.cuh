@@ -160,9 +160,13 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
     constexpr int NS = NT_ >= 128 ? 8 : 4;  // segments per value (threads per value)
     constexpr int SEG = NT_ / NS;           // partials per (value, segment)
     constexpr int L2N = SEG / 2;            // double2 loads per segment
-    const int tid = threadIdx.x;
+    // the reducers are the LAST 12 * NS threads (warps 1-3 at NT = 128), so
+    // warp 0, which builds the heaviest table (K) in the same window, is not
+    // on the reduction's critical path
+    constexpr int R0 = NT_ - 12 * NS > 0 ? ((NT_ - 12 * NS) & ~31) : 0;
+    const int tid = threadIdx.x - R0;
     // whole warps take part so the shuffles below are well defined
-    if ((tid & ~31) < 12 * NS) {
+    if (tid >= 0 && (tid & ~31) < 12 * NS) {
         const bool act = tid < 12 * NS;
         const int vid = act ? tid / NS : 0, seg = tid % NS;
         const double* src = sred + vid * NT_ + SEG * seg;
