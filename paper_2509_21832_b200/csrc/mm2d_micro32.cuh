@@ -97,37 +97,49 @@ enum { H_SCALE, H_WG, H_MTW, H_MEW, H_GQ12, H_WH, H_N = 8 };
 constexpr int HD = TAB;              // header offset inside a slot
 constexpr int SLOT = TAB + H_N;      // doubles per table slot
 
-// exp(x) to ~1 ulp for x <= 709 (Cody-Waite reduction by ln 2 and a
-// degree-13 Taylor polynomial on |r| <= ln2/2, truncation < 5e-18); results
+// exp(x) to ~1 ulp for x <= 709, table-driven: x = (64 m + i) ln2/64 + r
+// with |r| <= ln2/128 (Cody-Waite, two-part ln2/64), e^x = 2^m 2^(i/64) e^r,
+// e^r - 1 = r P(r) by a degree-5 Horner polynomial (truncation < 3e-20, each
+// step one DFMA with a constant-bank operand), 2^(i/64) from a 64-entry
+// shared-memory table (correctly rounded, generated at 60 digits).  Results
 // below ~1e-307 flush to zero (they only ever enter here as negligible
-// factors).  The coefficients live in the constant bank so every step is a
-// single DFMA: ~20 instructions against ~50 for libdevice exp.
-__constant__ double kExpC[14] = {   // 1/k!, k = 0..13
-    1.0, 1.0, 0.5, 1.6666666666666666667e-01, 4.1666666666666666667e-02,
-    8.3333333333333333333e-03, 1.3888888888888888889e-03, 1.9841269841269841270e-04,
-    2.4801587301587301587e-05, 2.7557319223985890653e-06, 2.7557319223985890653e-07,
-    2.5052108385441718775e-08, 2.0876756987868098979e-09, 1.6059043836821614599e-10};
-__constant__ double kLn2[3] = {1.4426950408889634074, 6.93147180559945286227e-01,
-                               2.31904681384629955842e-17};
+// factors).  ~20 instructions against ~40 for the previous polynomial-only
+// version and ~50 for libdevice exp.
+__constant__ double kExp2Tab[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
 
-__device__ __forceinline__ double fexp(double x) {
+__device__ __forceinline__ double fexp(double x, const double* etab) {
     const double SH = 6755399441055744.0;   // 1.5 * 2^52: round-to-int shifter
-    double t = fma(x, kLn2[0], SH);
+    double t = fma(x, 92.33248261689366, SH);            // x 64 / ln 2
     const int n = __double2loint(t);
     t -= SH;
-    double r = fma(t, -kLn2[1], x);
-    r = fma(t, -kLn2[2], r);
-    // Estrin evaluation: dependency depth 5 instead of 13
-    const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
-    const double q0 = fma(kExpC[1], r, kExpC[0]), q1 = fma(kExpC[3], r, kExpC[2]);
-    const double q2 = fma(kExpC[5], r, kExpC[4]), q3 = fma(kExpC[7], r, kExpC[6]);
-    const double q4 = fma(kExpC[9], r, kExpC[8]), q5 = fma(kExpC[11], r, kExpC[10]);
-    const double q6 = fma(kExpC[13], r, kExpC[12]);
-    const double s0 = fma(q1, r2, q0), s1 = fma(q3, r2, q2), s2 = fma(q5, r2, q4);
-    const double t0 = fma(s1, r4, s0), t1 = fma(q6, r4, s2);
-    const double p = fma(t1, r8, t0);
-    const int hi = __double2hiint(p) + (n << 20);
-    return n < -1020 ? 0.0 : __hiloint2double(hi, __double2loint(p));
+    double r = fma(t, -0.010830424696249145, x);         // ln2/64, high part
+    r = fma(t, -3.623510646634843e-19, r);               // ln2/64, low part
+    double p = fma(r, 1.3888888888888889e-03, 8.3333333333333333e-03);
+    p = fma(p, r, 4.1666666666666667e-02);
+    p = fma(p, r, 1.6666666666666667e-01);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    const double q = p * r;                               // e^r - 1
+    const double T = etab[n & 63];
+    const double e = fma(T, q, T);
+    const int hi = __double2hiint(e) + ((n >> 6) << 20);
+    return n < -1020 * 64 ? 0.0 : __hiloint2double(hi, __double2loint(e));
 }
 
 // Block all-reduce of the row's 12 sums (y | x | heat) through shared
@@ -203,7 +215,8 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
 // acc = M (U' + V' + c' W2 + q1' p2 + p1' q2) (+ the Gaussian) directly.
 template <int KS>
 __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, const CellPar& P,
-                                             const double* v1s, const double* v2s, bool gauss) {
+                                             const double* v1s, const double* v2s, bool gauss,
+                                             const double* etab) {
     const double mtw = -P.invtau * P.wh;
     for (int t = threadIdx.x; t < 128; t += blockDim.x) {
     const int m = t & 31;
@@ -216,11 +229,11 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         const double U = W1s * P.s11 * P.inv2T + q1 * p1;
         double* K = T + KT + 8 * m;
         sts2(K + K_W1N, w1, 0.5 * w1 * w1 - 1.0);
-        sts2(K + K_PE1, P.pref * fexp(-W1s * P.inv2T), W1);
+        sts2(K + K_PE1, P.pref * fexp(-W1s * P.inv2T, etab), W1);
         sts2(K + K_U, fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
              mtw * (2.0 * W1 * P.s12 * P.inv2T));
         sts2(K + K_Q1, mtw * q1, mtw * p1);
-        if (gauss) T[GK + 2 * m + 1] = fexp(P.gq12 * W1 * (v2s[1] - v2s[0]));
+        if (gauss) T[GK + 2 * m + 1] = fexp(P.gq12 * W1 * (v2s[1] - v2s[0]), etab);
         if (m == 0) {
             sts2(T + HD + H_SCALE, P.scale, P.wg);
             sts2(T + HD + H_MTW, mtw, a.inveps * P.wh);
@@ -233,20 +246,20 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         const double q2 = W2s * P.inv2T;
         const double p2 = W2 * P.gT2 * P.invT;
         double* L = T + LT + m;
-        L[L_E2 * NV] = fexp(-W2s * P.inv2T);
+        L[L_E2 * NV] = fexp(-W2s * P.inv2T, etab);
         L[L_W2N * NV] = w2;
         L[L_H2 * NV] = 0.5 * w2 * w2;
         L[L_W2 * NV] = W2;
         L[L_V * NV] = mtw * (q2 * p2 - W2s * P.s11 * P.inv2T);
         L[L_Q2 * NV] = q2;
         L[L_P2 * NV] = p2;
-        if (gauss) T[GL + NV + m] = fexp(P.gq12 * (v1s[KS] - v1s[0]) * W2);
+        if (gauss) T[GL + NV + m] = fexp(P.gq12 * (v1s[KS] - v1s[0]) * W2, etab);
     } else if (gauss && t < 96) {
         const double W1 = v1s[m] - P.u1;
-        T[GK + 2 * m] = P.gpref * a.inveps * P.wh * fexp(P.gq11 * (W1 * W1));
+        T[GK + 2 * m] = P.gpref * a.inveps * P.wh * fexp(P.gq11 * (W1 * W1), etab);
     } else if (gauss) {
         const double W2 = v2s[m] - P.u2;
-        T[GL + m] = fexp(P.gq22 * (W2 * W2));
+        T[GL + m] = fexp(P.gq22 * (W2 * W2), etab);
     }
     }
 }
@@ -292,7 +305,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 template <int NP_>
 inline size_t smem_bytes_v3() {
     constexpr int NT_ = 512 / NP_;
-    return sizeof(double) * (3 * V + 2 * V + TSLOTS * SLOT + red_size<NT_>() + 4 * 32 + 2 * NV + 2);
+    return sizeof(double) * (3 * V + 2 * V + TSLOTS * SLOT + red_size<NT_>() + 4 * 32 + 2 * NV + 2 + 64);
 }
 
 // The host selects this kernel only when the velocity axes make the upwind
@@ -326,8 +339,10 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
     double* pring = sred + red_size<NT_>();         // [4][32] staged CellPar rows
     double* v1s = pring + 4 * 32;
     double* v2s = v1s + NV;
+    double* etab = v2s + NV + 2;                    // [64] 2^(i/64)
     if (tid < NV) v1s[tid] = a.v1[tid];
     else if (tid < 2 * NV) v2s[tid - NV] = a.v2[tid - NV];
+    if (tid < 64) etab[tid] = kExp2Tab[tid];
 
     const bool gauss = a.gauss && !(a.eps < 1e-10 &&
         __longlong_as_double(a.iso[0]) <= 1e-13 * __longlong_as_double(a.iso[3]) &&
@@ -566,7 +581,7 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         // the opening barrier above
         if (ST || computes(j + 3))
             build_tables<KS>(a, T3, *reinterpret_cast<const CellPar*>(pring + 32 * ((j + 3) & 3)),
-                             v1s, v2s, gauss);
+                             v1s, v2s, gauss, etab);
         // target + Gaussian of row j: independent of the projection sums, so
         // it is evaluated inside the reduction window
         double acc[2 * NP_];
@@ -586,7 +601,7 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
                 if (gauss) {
                     GB = lds2(T + GL + lb);
                     GR = T[GL + NV + lb];
-                    Xp = fexp(T[HD + H_GQ12] * T[KT + 8 * kb + K_W1] * W2.x);
+                    Xp = fexp(T[HD + H_GQ12] * T[KT + 8 * kb + K_W1] * W2.x, etab);
                 }
 #pragma unroll
                 for (int p = 0; p < NP_; ++p) {
