@@ -228,14 +228,9 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         }
     }
     if (ctx->use32) {
-        const char* np = getenv("MM2D_NP");
-        ctx->np32 = np ? atoi(np) : 4;
-        if (ctx->np32 != 2 && ctx->np32 != 8) ctx->np32 = 4;
-        const void* fn = ctx->np32 == 2 ? reinterpret_cast<const void*>(&m32::k_micro32<2>)
-                         : ctx->np32 == 8 ? reinterpret_cast<const void*>(&m32::k_micro32<8>)
-                                          : reinterpret_cast<const void*>(&m32::k_micro32<4>);
-        const size_t sm = ctx->np32 == 2 ? m32::smem_bytes_v3<2>()
-                          : ctx->np32 == 8 ? m32::smem_bytes_v3<8>() : m32::smem_bytes_v3<4>();
+        ctx->np32 = 4;
+        const void* fn = reinterpret_cast<const void*>(&m32::k_micro32<4>);
+        const size_t sm = m32::smem_bytes_v3<4>();
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm) != cudaSuccess) {
             int r = fail_cfg(ctx, "shared memory request too large for k_micro32");
@@ -243,7 +238,7 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
             return r;
         }
         int occ = 0, nsm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 512 / ctx->np32, sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, sm);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
         // Band height: a CTA walks one column through ly rows, paying ~4
         // pipeline-fill iterations per band.  Measured on C2 (256 x 256,
@@ -417,12 +412,7 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
         }
         ma.ly = ctx->ly32;
         dim3 grid(g.bx, (g.by + ctx->ly32 - 1) / ctx->ly32);
-        if (ctx->np32 == 2)
-            m32::k_micro32<2><<<grid, 256, m32::smem_bytes_v3<2>(), s>>>(ma);
-        else if (ctx->np32 == 8)
-            m32::k_micro32<8><<<grid, 64, m32::smem_bytes_v3<8>(), s>>>(ma);
-        else
-            m32::k_micro32<4><<<grid, 128, m32::smem_bytes_v3<4>(), s>>>(ma);
+        m32::k_micro32<4><<<grid, 128, m32::smem_bytes_v3<4>(), s>>>(ma);
     } else {
         dim3 grid((g.bx + ctx->BX - 1) / ctx->BX, (g.by + ctx->ly - 1) / ctx->ly);
         void* args[] = {&ma};

@@ -28,6 +28,12 @@
 #include "mm2d_common.cuh"
 #include "mm2d_micro.cuh"
 
+#ifndef MICRO32_MINB
+#define MICRO32_MINB 3   // resident CTAs per SM the register budget is sized for (4 fits
+                         // the 52 KB of shared memory but spills at 128 registers and is
+                         // 11% slower)
+#endif
+
 namespace mm2d {
 namespace m32 {
 
@@ -302,10 +308,46 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
 }
 
+// Thread-private rows in tensor memory.  A warp may only touch its own
+// 32-lane quadrant, and every thread its own lane, which is exactly the
+// access pattern of the thread-private G* ring: 8 doubles of a thread's row
+// are 16 consecutive 32-bit columns of its lane, moved by ONE
+// tcgen05.ld/st .32x32b.x16 (against four 16-byte LDS/STS in shared memory).
+__device__ __forceinline__ void tm_st8(unsigned addr, const double (&v)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, "
+        "%10, %11, %12, %13, %14, %15, %16};\n" ::"r"(addr),
+        "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])),
+        "r"(__double2hiint(v[1])), "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])),
+        "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])), "r"(__double2loint(v[4])),
+        "r"(__double2hiint(v[4])), "r"(__double2loint(v[5])), "r"(__double2hiint(v[5])),
+        "r"(__double2loint(v[6])), "r"(__double2hiint(v[6])), "r"(__double2loint(v[7])),
+        "r"(__double2hiint(v[7]))
+        : "memory");
+}
+__device__ __forceinline__ void tm_ld8(unsigned addr, double (&v)[8]) {
+    int r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(addr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __hiloint2double(r[2 * q + 1], r[2 * q]);
+}
+__device__ __forceinline__ void tm_wait_st() {
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+constexpr int TM_COLS = 64;          // 3 rows x 16 columns, rounded to a power of two
+
 template <int NP_>
 inline size_t smem_bytes_v3() {
     constexpr int NT_ = 512 / NP_;
-    return sizeof(double) * (3 * V + 2 * V + TSLOTS * SLOT + red_size<NT_>() + 4 * 32 + 2 * NV + 2 + 64);
+    return sizeof(double) * (2 * V + TSLOTS * SLOT + red_size<NT_>() + 4 * 32 + 2 * NV + 2 + 64 + 2);
 }
 
 // The host selects this kernel only when the velocity axes make the upwind
@@ -323,17 +365,22 @@ inline size_t smem_bytes_v3() {
 // thread's W2 powers.  The row loop runs a predicate-free body for the rows
 // away from the piece ends.
 template <int NP_>
-__global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_micro32(MicroArgs a) {
+__global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a) {
+    static_assert(NP_ == 4, "the TMEM ring is laid out for 4 node pairs per thread");
     constexpr int NT_ = 512 / NP_;       // threads per CTA
     constexpr int KS = 32 / NP_;         // k step between a thread's node pairs
     extern __shared__ __align__(16) double smem[];
     const Geometry& g = a.g;
     if (*a.err != kNoError) return;
     const int tid = threadIdx.x;
-    const int kb = tid >> 4, lb = (tid & 15) << 1;
+    // thread -> nodes: l pair lp, k base kb.  Warps 0/2 take the v2 < 0 half
+    // (l < 16), warps 1/3 the v2 >= 0 half, so the y-upwind direction is
+    // warp-uniform (the TMEM ring's loads are warp-collective).
+    const int lp = (tid & 7) + 8 * ((tid >> 5) & 1);
+    const int kb = ((tid >> 3) & 3) + 4 * (tid >> 6);
+    const int lb = lp << 1;
 
-    double* ring = smem;                            // [3][V]
-    double* stg = ring + 3 * V;                     // [2][V] x-stage row: own | halo
+    double* stg = smem;                             // [2][V] x-stage row: own | halo
     double* tabs = stg + 2 * V;                     // [TSLOTS][SLOT]
     double* sred = tabs + TSLOTS * SLOT;            // [12][NT] partials + [12] totals
     double* pring = sred + red_size<NT_>();         // [4][32] staged CellPar rows
@@ -426,7 +473,20 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         mbar_init(mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    // the G* ring: 64 TMEM columns, allocated by warp 0
+    unsigned* tslot = reinterpret_cast<unsigned*>(etab + 64);
+    if (tid < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(tslot)),
+                     "n"(TM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const unsigned tbase = *reinterpret_cast<volatile unsigned*>(tslot);
+    const unsigned tq = tbase + ((unsigned)(tid & ~31) << 16);   // this warp's lane quadrant
     unsigned nload = 0;            // bulk loads issued (mbarrier phase = parity)
     auto prefetch = [&](int r, auto steady) {
         if (tid != 0) { ++nload; return; }
@@ -453,9 +513,7 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
 
     // rotating slot pointers: ring rows (j-1, j, j+1); table rows
     // (j, j+1, j+2, j+3, j-1)
-    double* R0 = ring;
-    double* R1 = ring + V;
-    double* R2 = ring + 2 * V;
+    unsigned R0 = tq, R1 = tq + 16, R2 = tq + 32;   // TMEM ring rows (j-1, j, j+1)
     double* T0 = tabs;
     double* T1 = tabs + SLOT;
     double* T2 = tabs + 2 * SLOT;
@@ -501,7 +559,10 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         // 0. stage the CellPar of row j+5 (its tables are built two
         //    iterations from now)
         stage_par(j + 5, ST || computes(j + 5));
-        // 1. recon G*(j+1) = (G - dt Z) + dt Zhat_x
+        // 1. recon G*(j+1) = (G - dt Z) + dt Zhat_x (kept in gst for the
+        //    v2 < 0 warps' y-stage, stored to the ring for the others)
+        double gst[2 * NP_];
+        tm_wait_st();
         if (ST || computes(rc)) {
             const double* T = T1;
             const double sc = T[HD + H_SCALE];
@@ -511,46 +572,45 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             const double bE0 = fma(w2.x, a3, h2.x * a4) * E2.x;
             const double bE1 = fma(w2.y, a3, h2.y * a4) * E2.y;
+            tm_ld8(R2, gst);
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
                 const double2 wh = lds2(T + koff_(p) + K_W1N);   // w1, h1
                 const double pe = T[koff_(p) + K_PE1];
                 const double alp = fma(wh.x, a2, fma(wh.y, a4, a1)) * pe;
-                const double2 t = lds2(R2 + off_(p));
-                sts2(R2 + off_(p), fma(alp, E2.x, fma(bE0, pe, t.x)),
-                     fma(alp, E2.y, fma(bE1, pe, t.y)));
+                gst[2 * p] = fma(alp, E2.x, fma(bE0, pe, gst[2 * p]));
+                gst[2 * p + 1] = fma(alp, E2.y, fma(bE1, pe, gst[2 * p + 1]));
             }
+            tm_st8(R2, gst);
         } else if ((rc == j1s && k_hi != 0) || (rc == j0s - 1 && k_lo == 2)) {
             // ghost rows: zero (wall) or copy of the adjacent owned row
-            const bool cp = rc == j1s && k_hi == 1;
+            if (rc == j1s && k_hi == 1) tm_ld8(R1, gst);
+            else {
 #pragma unroll
-            for (int p = 0; p < NP_; ++p) {
-                const double2 s = cp ? lds2(R1 + off_(p)) : make_double2(0.0, 0.0);
-                sts2(R2 + off_(p), s.x, s.y);
+                for (int q = 0; q < 2 * NP_; ++q) gst[q] = 0.0;
             }
+            tm_st8(R2, gst);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 2 * NP_; ++q) gst[q] = 0.0;
         }
         if (!ST && rc == j0s && k_lo == 1) {   // bottom ghost by copy, once G*(j0s) is complete
-#pragma unroll
-            for (int p = 0; p < NP_; ++p) {
-                const double2 s = lds2(R2 + off_(p));
-                sts2(R1 + off_(p), s.x, s.y);
-            }
+            tm_wait_st();
+            tm_st8(R1, gst);
         }
         double s[12];
 #pragma unroll
         for (int q = 0; q < 8; ++q) s[q] = 0.0;
         // 2. y-sums of row j: Y = cy (G*_j - G*_upwind)
         if (row_j) {
-            const double* gn = negy ? R2 : R0;
-            double y[2 * NP_];
+            if (!ST) tm_wait_st();         // the bottom-ghost copy may have just written R1
+            double c[2 * NP_], y[2 * NP_];
+            tm_ld8(R1, c);
+            if (!negy) tm_ld8(R0, gst);     // warp-uniform; v2 < 0 warps use G*(j+1) = gst
 #pragma unroll
-            for (int p = 0; p < NP_; ++p) {
-                const double2 c = lds2(R1 + off_(p));
-                const double2 n = lds2(gn + off_(p));
-                y[2 * p] = cy0 * (c.x - n.x);
-                y[2 * p + 1] = cy1 * (c.y - n.y);
-                ty[2 * p] = c.x - y[2 * p];
-                ty[2 * p + 1] = c.y - y[2 * p + 1];
+            for (int q = 0; q < 2 * NP_; ++q) {
+                y[q] = ((q & 1) ? cy1 : cy0) * (c[q] - gst[q]);
+                ty[q] = c[q] - y[q];
             }
             stage_sums(T0, y, s);
         }
@@ -558,14 +618,16 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         const bool do_x = ST || computes(rx);
         if (do_x) {
             mbar_wait(mbar, (nload - 1) & 1);   // this row's bulk loads (issued one iteration ago)
-            double y[2 * NP_];
+            double y[2 * NP_], xs[2 * NP_];
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
                 const double2 c = lds2(stg + off_(p)), h = lds2(stg + V + off_(p));
                 y[2 * p] = cx[p] * (c.x - h.x);
                 y[2 * p + 1] = cx[p] * (c.y - h.y);
-                sts2(R0 + off_(p), c.x - y[2 * p], c.y - y[2 * p + 1]);
+                xs[2 * p] = c.x - y[2 * p];
+                xs[2 * p + 1] = c.y - y[2 * p + 1];
             }
+            tm_st8(R0, xs);
             stage_sums(T2, y, s + 4);
         }
         s[8] = hs[0]; s[9] = hs[1]; s[10] = hs[2]; s[11] = hs[3];
@@ -683,7 +745,7 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
         }
         // rotate slots for the next row
         {
-            double* r0 = R0; R0 = R1; R1 = R2; R2 = r0;
+            const unsigned r0 = R0; R0 = R1; R1 = R2; R2 = r0;
             double* t0 = T0; T0 = T1; T1 = T2; T2 = T3; T3 = t0;
         }
     };
@@ -694,6 +756,15 @@ __global__ void __launch_bounds__(512 / NP_, NP_ == 8 ? 4 : NP_ == 4 ? 3 : 2) k_
     for (; j < js_lo && j <= j1s; ++j) body(j, std::false_type());
     for (; j <= js_hi; ++j) body(j, std::true_type());
     for (; j <= j1s; ++j) body(j, std::false_type());
+    // release the ring (every warp's TMEM traffic has completed)
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (tid < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase),
+                     "n"(TM_COLS)
+                     : "memory");
 #undef off_
 #undef koff_
 }
