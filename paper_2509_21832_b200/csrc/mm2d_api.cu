@@ -390,6 +390,7 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     pa.tau_kind = c.tau_kind; pa.tau_value = c.tau_value;
     pa.step = 0;
     pa.gauss = gauss;
+    pa.h2x = 0.5 / g.dx; pa.h2y = 0.5 / g.dy;
     k_prep<<<grid_for(ring, 128), 128, 0, s>>>(pa);
     MARK(2);
     MicroArgs ma;

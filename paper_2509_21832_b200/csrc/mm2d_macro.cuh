@@ -35,7 +35,7 @@ struct MacroArgs {
 // relax_pressure_2d (macro2d.py:55-70) on one cell
 __device__ __forceinline__ void relax_cell(const MacroArgs& a, const double* q, double* o) {
     double rho, u1, u2, t11, t12, t22;
-    prims_of(q, rho, u1, u2, t11, t12, t22);
+    prims_fast(q, rho, u1, u2, t11, t12, t22);
     const double T = 0.5 * (t11 + t22);
     const double tau = tau_model(a.tau_kind, a.tau_value, rho, T);
     const double z = tau * (1.0 - a.nu) * a.dt;
@@ -52,7 +52,7 @@ __device__ __forceinline__ void relax_cell(const MacroArgs& a, const double* q, 
 // vector (_pressure_fields, macro2d.py:201-203)
 __device__ __forceinline__ void pstate(const double* q, double* s) {
     double rho, u1, u2, t11, t12, t22;
-    prims_of(q, rho, u1, u2, t11, t12, t22);
+    prims_fast(q, rho, u1, u2, t11, t12, t22);
     s[0] = rho; s[1] = u1; s[2] = u2;
     s[3] = rho * t11; s[4] = rho * t12; s[5] = rho * t22;
 }
@@ -87,22 +87,28 @@ template <int AXIS>
 __device__ __forceinline__ void kfvs_half(const double* s, double sgn, double* out) {
     const double rho = s[0], u1 = s[1], u2 = s[2], p11 = s[3], p12 = s[4], p22 = s[5];
     double a, b, J[6], K[6];
+    // two divisions per half (1/rho, 1/P_aa) instead of four
+    const double irho = 1.0 / rho;
     if (AXIS == 0) {
-        a = sqrt(2.0 * p11 / (kPi * rho)) * exp(-rho * u1 * u1 / (2.0 * p11));
-        b = erf(u1 * sqrt(rho / (2.0 * p11)));
+        const double rp = 1.0 / p11;
+        const double h = 0.5 * rho * rp;         // rho / (2 P11)
+        a = sqrt((2.0 / kPi) * p11 * irho) * exp(-u1 * u1 * h);
+        b = erf(u1 * sqrt(h));
         J[0] = rho; J[1] = rho * u1; J[2] = rho * u2;
         J[3] = rho * u1 * u1 + 2.0 * p11;
         J[4] = rho * u1 * u2 + 2.0 * p12;
-        J[5] = rho * u2 * u2 + p22 + p12 * p12 / p11;
+        J[5] = rho * u2 * u2 + p22 + p12 * p12 * rp;
         K[0] = rho * u1; K[1] = rho * u1 * u1 + p11; K[2] = rho * u1 * u2 + p12;
         K[3] = rho * (u1 * u1 * u1) + 3.0 * u1 * p11;
         K[4] = rho * u1 * u1 * u2 + u2 * p11 + 2.0 * u1 * p12;
         K[5] = rho * u1 * u2 * u2 + u1 * p22 + 2.0 * u2 * p12;
     } else {
-        a = sqrt(2.0 * p22 / (kPi * rho)) * exp(-rho * u2 * u2 / (2.0 * p22));
-        b = erf(u2 * sqrt(rho / (2.0 * p22)));
+        const double rp = 1.0 / p22;
+        const double h = 0.5 * rho * rp;         // rho / (2 P22)
+        a = sqrt((2.0 / kPi) * p22 * irho) * exp(-u2 * u2 * h);
+        b = erf(u2 * sqrt(h));
         J[0] = rho; J[1] = rho * u1; J[2] = rho * u2;
-        J[3] = rho * u1 * u1 + p11 + p12 * p12 / p22;
+        J[3] = rho * u1 * u1 + p11 + p12 * p12 * rp;
         J[4] = rho * u1 * u2 + 2.0 * p12;
         J[5] = rho * u2 * u2 + 2.0 * p22;
         K[0] = rho * u2; K[1] = rho * u1 * u2 + p12; K[2] = rho * u2 * u2 + p22;

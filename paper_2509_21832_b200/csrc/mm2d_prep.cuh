@@ -98,6 +98,7 @@ struct PrepArgs {
     double tau_value;
     unsigned step;
     int gauss;                    // nu != 0
+    double h2x, h2y;              // 1 / (2 dx), 1 / (2 dy)
 };
 
 __device__ __forceinline__ double tau_model(int kind, double value, double rho, double T) {
@@ -128,6 +129,21 @@ __device__ __forceinline__ void prims_of(const double* q, double& rho, double& u
     t22 = q[5] / rho - u2 * u2;
 }
 
+// Primitives with one reciprocal of rho instead of five divisions (~1 ulp
+// from prims_of).  Used where the result only feeds the evolution (neighbour
+// gradients, relaxation, KFVS states); every validity check and every
+// reported InvalidStateError value goes through the exact prims_of.
+__device__ __forceinline__ void prims_fast(const double* q, double& rho, double& u1, double& u2,
+                                           double& t11, double& t12, double& t22) {
+    rho = q[0];
+    const double ir = 1.0 / rho;
+    u1 = q[1] * ir;
+    u2 = q[2] * ir;
+    t11 = q[3] * ir - u1 * u1;
+    t12 = q[4] * ir - u1 * u2;
+    t22 = q[5] * ir - u2 * u2;
+}
+
 // Per ring cell: primitives, tau, Maxwellian and Gaussian prefactors, relax
 // weights; per owned cell also the centred gradients (micro2d.py:37-60),
 // the modified tensor with its SPD check (gas_state.py:138-146), the
@@ -156,17 +172,20 @@ __global__ void k_prep(PrepArgs a) {
         }
         P.rho = rho; P.u1 = u1; P.u2 = u2; P.T = T;
         P.t11 = t11; P.t12 = t12; P.t22 = t22;
-        P.isT = 1.0 / sqrt(T);
-        P.invT = 1.0 / T;
-        P.inv2T = 1.0 / (2.0 * T);
-        P.pref = rho / (2.0 * kPi * T);
+        // reciprocals shared between the derived constants (each division
+        // costs ~40 instructions with its slow-path guard)
+        const double invT = 1.0 / T;
+        P.isT = rsqrt(T);
+        P.invT = invT;
+        P.inv2T = 0.5 * invT;                   // == 1 / (2T) exactly
+        P.pref = rho * invT * (0.5 / kPi);
         const double tau = tau_model(a.tau_kind, a.tau_value, rho, T);
         P.tau = tau;
         P.invtau = 1.0 / tau;
         P.scale = a.dv / rho;
-        const double denom = a.eps + a.dt * tau;
-        P.wg = a.eps / denom;
-        P.wh = a.dt * tau / denom;
+        const double rden = 1.0 / (a.eps + a.dt * tau);
+        P.wg = a.eps * rden;
+        P.wh = a.dt * tau * rden;
         P.s11 = P.s12 = P.gT1 = P.gT2 = 0.0;
         P.m11 = P.m12 = P.m22 = 0.0;
         P.gpref = P.gq11 = P.gq22 = P.gq12 = 0.0;
@@ -177,11 +196,12 @@ __global__ void k_prep(PrepArgs a) {
             const double m12 = a.nu * t12;
             const double m22 = (1.0 - a.nu) * T + a.nu * t22;
             const double det = m11 * m22 - m12 * m12;
+            const double rdet = 1.0 / det;
             P.m11 = m11; P.m12 = m12; P.m22 = m22;
-            P.gpref = rho / (2.0 * kPi * sqrt(det));
-            P.gq11 = -0.5 * m22 / det;   // coefficient of W1^2 in the exponent
-            P.gq22 = -0.5 * m11 / det;   // coefficient of W2^2
-            P.gq12 = m12 / det;          // coefficient of W1 W2
+            P.gpref = rho * (0.5 / kPi) * rsqrt(det);
+            P.gq11 = -0.5 * m22 * rdet;  // coefficient of W1^2 in the exponent
+            P.gq22 = -0.5 * m11 * rdet;  // coefficient of W2^2
+            P.gq12 = m12 * rdet;         // coefficient of W1 W2
             if (own) {
                 const double tol = 1e-14 * (m11 + m22);
                 if ((m11 <= tol) || (det <= tol * tol))
@@ -201,20 +221,20 @@ __global__ void k_prep(PrepArgs a) {
             double a11, a12, a22;
             for (int s = 0; s < 2; ++s) {
                 const double* qx = a.Qr + 6 * ring_index(g, i + (s ? 1 : -1), j);
-                prims_of(qx, r_, xu1[s], xu2[s], a11, a12, a22);
+                prims_fast(qx, r_, xu1[s], xu2[s], a11, a12, a22);
                 xT[s] = 0.5 * (a11 + a22);
                 const double* qy = a.Qr + 6 * ring_index(g, i, j + (s ? 1 : -1));
-                prims_of(qy, r_, yu1[s], yu2[s], a11, a12, a22);
+                prims_fast(qy, r_, yu1[s], yu2[s], a11, a12, a22);
                 yT[s] = 0.5 * (a11 + a22);
             }
-            const double du1x = (xu1[1] - xu1[0]) / (2.0 * g.dx);
-            const double du2x = (xu2[1] - xu2[0]) / (2.0 * g.dx);
-            const double du1y = (yu1[1] - yu1[0]) / (2.0 * g.dy);
-            const double du2y = (yu2[1] - yu2[0]) / (2.0 * g.dy);
+            const double du1x = (xu1[1] - xu1[0]) * a.h2x;
+            const double du2x = (xu2[1] - xu2[0]) * a.h2x;
+            const double du1y = (yu1[1] - yu1[0]) * a.h2y;
+            const double du2y = (yu2[1] - yu2[0]) * a.h2y;
             P.s11 = du1x - du2y;
             P.s12 = du1y + du2x;
-            P.gT1 = (xT[1] - xT[0]) / (2.0 * g.dx);
-            P.gT2 = (yT[1] - yT[0]) / (2.0 * g.dy);
+            P.gT1 = (xT[1] - xT[0]) * a.h2x;
+            P.gT2 = (yT[1] - yT[0]) * a.h2y;
             // wall ghost densities of edge cells (zero-mass-flux closure)
             if (g.wall[0] && i == 0) P.rw[0] = wall_density(rho, u1, t11, g.wallT[0], -1.0);
             if (g.wall[1] && i == g.bx - 1) P.rw[1] = wall_density(rho, u1, t11, g.wallT[1], 1.0);
