@@ -314,30 +314,31 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // are 16 consecutive 32-bit columns of its lane, moved by ONE
 // tcgen05.ld/st .32x32b.x16 (against four 16-byte LDS/STS in shared memory).
 __device__ __forceinline__ void tm_st8(unsigned addr, const double (&v)[8]) {
+    // the doubles are split inside PTX so ptxas can place them straight into
+    // the 16 consecutive registers STTM reads
     asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, "
-        "%10, %11, %12, %13, %14, %15, %16};\n" ::"r"(addr),
-        "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])),
-        "r"(__double2hiint(v[1])), "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])),
-        "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])), "r"(__double2loint(v[4])),
-        "r"(__double2hiint(v[4])), "r"(__double2loint(v[5])), "r"(__double2hiint(v[5])),
-        "r"(__double2loint(v[6])), "r"(__double2hiint(v[6])), "r"(__double2loint(v[7])),
-        "r"(__double2hiint(v[7]))
+        "{\n .reg .b32 a<16>;\n"
+        " mov.b64 {a0, a1}, %1;\n mov.b64 {a2, a3}, %2;\n mov.b64 {a4, a5}, %3;\n"
+        " mov.b64 {a6, a7}, %4;\n mov.b64 {a8, a9}, %5;\n mov.b64 {a10, a11}, %6;\n"
+        " mov.b64 {a12, a13}, %7;\n mov.b64 {a14, a15}, %8;\n"
+        " tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, "
+        "a10, a11, a12, a13, a14, a15};\n}\n" ::"r"(addr),
+        "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]), "d"(v[4]), "d"(v[5]), "d"(v[6]), "d"(v[7])
         : "memory");
 }
 __device__ __forceinline__ void tm_ld8(unsigned addr, double (&v)[8]) {
-    int r[16];
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-        "%11, %12, %13, %14, %15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        "{\n .reg .b32 a<16>;\n"
+        " tcgen05.ld.sync.aligned.32x32b.x16.b32 {a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, "
+        "a11, a12, a13, a14, a15}, [%8];\n"
+        " tcgen05.wait::ld.sync.aligned;\n"
+        " mov.b64 %0, {a0, a1};\n mov.b64 %1, {a2, a3};\n mov.b64 %2, {a4, a5};\n"
+        " mov.b64 %3, {a6, a7};\n mov.b64 %4, {a8, a9};\n mov.b64 %5, {a10, a11};\n"
+        " mov.b64 %6, {a12, a13};\n mov.b64 %7, {a14, a15};\n}\n"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]),
+          "=d"(v[7])
         : "r"(addr)
         : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = __hiloint2double(r[2 * q + 1], r[2 * q]);
 }
 __device__ __forceinline__ void tm_wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
