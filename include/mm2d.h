@@ -142,6 +142,13 @@ int mm2d_state_ptrs(mm2d_ctx *ctx, double **d_Q, double **d_G, double **d_H);
 int mm2d_heat_tensor(mm2d_ctx *ctx, const double *d_G, const double *d_Q,
                      double *d_H, void *stream);
 
+/* steady-state tracking of the run driver (runner/cases.py:217-222,
+ * max |Q^{n+1} - Q^n| over the last 10% of steps): *d_max = max(*d_max,
+ * max_k |a_k - b_k|) over n doubles, on the device (no host sync).  *d_max
+ * must start non-negative (e.g. 0). */
+int mm2d_max_abs_diff(mm2d_ctx *ctx, const double *d_a, const double *d_b, long long n,
+                      double *d_max, void *stream);
+
 /* synchronise and report the sticky device error word.  Returns MM2D_OK or
  * MM2D_ERR_STATE with *kind = MM2D_STATE_*, (*i, *j) the global cell and
  * *value the offending value (density or determinant). */

@@ -92,6 +92,7 @@ SIGNATURES = {
     "mm2d_check": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                              C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "mm2d_sync": (C.c_int, [_vp]),
+    "mm2d_max_abs_diff": (C.c_int, [_vp, _vp, _vp, C.c_longlong, _vp, _vp]),
     "mm2d_halo_info": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(_vp), C.POINTER(_vp),
                                  C.POINTER(C.c_longlong)]),
     "mm2d_halo_pack": (C.c_int, [_vp, C.c_int, _vp, _vp]),

@@ -674,6 +674,29 @@ extern "C" int mm2d_heat_tensor(mm2d_ctx* ctx, const double* d_G, const double* 
     return MM2D_OK;
 }
 
+// max |a - b| accumulated into *out (non-negative doubles order like their
+// bit patterns, so an unsigned atomicMax is an exact max)
+__global__ void k_max_abs_diff(const double* a, const double* b, long long n, double* out) {
+    double m = 0.0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x)
+        m = fmax(m, fabs(a[t] - b[t]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0)
+        atomic_max_pos(reinterpret_cast<unsigned long long*>(out), m);
+}
+
+extern "C" int mm2d_max_abs_diff(mm2d_ctx* ctx, const double* d_a, const double* d_b, long long n,
+                                 double* d_max, void* stream) {
+    if (!ctx || !d_a || !d_b || !d_max || n < 0) return fail_cfg(ctx, "max_abs_diff arguments");
+    CK(cudaSetDevice(ctx->dev));
+    if (n == 0) return MM2D_OK;
+    k_max_abs_diff<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(d_a, d_b, n, d_max);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    return MM2D_OK;
+}
+
 extern "C" int mm2d_sync(mm2d_ctx* ctx) {
     if (!ctx) return MM2D_ERR_CONFIG;
     CK(cudaSetDevice(ctx->dev));

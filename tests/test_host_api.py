@@ -109,3 +109,22 @@ def test_device_path_fails_loudly_without_gpu():
     st = State2D(0.0, conserved_2d(np.ones((4, 4)), 0, 0, 1, 0, 1), np.zeros((4, 4, 4, 4)))
     with pytest.raises(NativeLibraryError):
         step_2d(st, mesh, bc, 0.1, CollisionModel("esbgk_2d"), 1e-3)
+
+
+def test_run_driver_host_helpers():
+    """snap-step mapping, steady window and totals follow cases.py:178-222."""
+    from paper_2509_21832_b200.runner.drive import snap_steps, steady_window, totals
+    # nearest step, clipped to [1, n], first request wins; Python round (half to even)
+    assert snap_steps([0.01, 0.011, 0.5, 2.0, 0.0], 0.004, 100) == {2: 0.01, 3: 0.011, 100: 0.5, 1: 0.0}
+    assert snap_steps([0.01, 0.0101], 0.004, 100) == {2: 0.01, 3: 0.0101}
+    assert steady_window(7) == 1 and steady_window(100) == 10 and steady_window(101) == 11
+    Q = np.arange(2 * 3 * 6, dtype=float).reshape(2, 3, 6)
+    assert totals(Q, 0.5) == tuple(float(v) for v in Q.reshape(-1, 6).sum(axis=0) * 0.5)
+
+
+def test_heat_flux_vector_matches_reference_formula():
+    from paper_2509_21832_b200.macro2d import heat_flux_vector_2d
+    rng = np.random.default_rng(3)
+    h = rng.normal(size=(4, 5, 6))
+    hx, hy = heat_flux_vector_2d(*h)
+    assert np.array_equal(hx, 0.5 * (h[0] + h[2])) and np.array_equal(hy, 0.5 * (h[1] + h[3]))
