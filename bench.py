@@ -311,8 +311,16 @@ def run_ours_multi(args, rank, world, local_rank):
     from paper_2509_21832_b200 import _native
     from paper_2509_21832_b200.parallel import (BlockStepper, DistExchange, make_plans,
                                                 step_blocks)
+    gloo = args.backend == "gloo"
+    if gloo:
+        # functional check of the multi-rank path on fewer GPUs than ranks:
+        # exchanges go through pinned host memory, no kernel waits on another rank
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if gloo:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     px, py = rank_grid(world)
     cfg_name = args.config or "c2"
     cfg = make_workload(cfg_name, px=px, py=py)
@@ -320,7 +328,7 @@ def run_ours_multi(args, rank, world, local_rank):
     plan = make_plans(nx, ny, (px, py), cfg["bc"])[rank]
     blk = BlockStepper(cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"], (px, py), plan,
                        torch.device("cuda", local_rank))
-    exch = DistExchange(plan, blk.bufs)
+    exch = DistExchange(plan, blk.bufs, staged=gloo)
     lib = _native.load()
     bx, by = plan.shape
     Q = torch.from_numpy(cfg["initial"](plan.i0, plan.i1, plan.j0, plan.j1)).cuda()
@@ -355,7 +363,7 @@ def run_ours_multi(args, rank, world, local_rank):
     tw1 = time.time()
     launches = int(lib.mm2d_launch_count())
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device="cuda")
+    t = torch.tensor([ms], device="cpu" if gloo else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     dist.barrier()
@@ -388,7 +396,7 @@ def run_ours_multi(args, rank, world, local_rank):
         Ho.copy_(st[4], non_blocking=True)
     f1.record(stream)
     torch.cuda.synchronize()
-    t = torch.tensor([f0.elapsed_time(f1) / n_e2e], device="cuda")
+    t = torch.tensor([f0.elapsed_time(f1) / n_e2e], device="cpu" if gloo else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
     line = {
@@ -398,7 +406,9 @@ def run_ours_multi(args, rank, world, local_rank):
         "data": "synthetic (BASELINE config initial conditions, g=0)",
         "config": {"workload": cfg["workload"], "nx": nx, "ny": ny, "nv1": 32, "nv2": 32,
                    "dt": dt, "parallelism": f"dd{px}x{py}",
-                   "exchange": "NCCL send/recv (torch.distributed), G+Q ring and heat ring per step",
+                   "exchange": ("gloo via pinned host (functional test only)" if gloo else
+                                "NCCL send/recv (torch.distributed)") +
+                               ", G+Q ring and heat ring per step",
                    "l2": "inputs larger than L2 (G per GPU = %.0f MiB)" % (bx * by * V * 8 / 2**20)},
         "roofline": {"bound": "hbm", "kernel": "full decomposed step",
                      "achieved": step_gbs / world, "peak": peak, "unit": "GB/s",
@@ -597,6 +607,8 @@ def main():
     ap.add_argument("--config", default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional test of the multi-rank path on fewer GPUs than ranks")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", 0))

@@ -123,30 +123,52 @@ class DistExchange:
     is inactive).  Sends are posted in slot order and receives in slot order
     of the opposite direction, so the matching between any pair of ranks is
     well defined even when one neighbour occupies several slots (periodic
-    wrap over two blocks)."""
+    wrap over two blocks).
 
-    def __init__(self, plan: HaloPlan, bufs, group=None):
+    With ``staged=True`` (a backend without device P2P, e.g. gloo driving
+    device buffers in tests) every slot goes through pinned host mirrors."""
+
+    def __init__(self, plan: HaloPlan, bufs, group=None, staged=False):
         self.plan = plan
         self.bufs = bufs
         self.group = group
+        self.staged = staged
+        self._host = {}
+
+    def _mirror(self, t):
+        key = t.data_ptr()
+        if key not in self._host:
+            import torch
+            self._host[key] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        return self._host[key]
 
     def exchange(self, field):
         import torch.distributed as dist
-        ops = []
+        ops, back = [], []
         for s in range(8):
             peer = self.plan.slots[s]
             send, _ = self.bufs[field][s]
             if peer is not None and send is not None:
+                if self.staged:
+                    h = self._mirror(send)
+                    h.copy_(send)
+                    send = h
                 ops.append(dist.P2POp(dist.isend, send, peer, self.group))
         for s in range(8):
             o = OPPOSITE[s]
             peer = self.plan.slots[o]
             _, recv = self.bufs[field][o]
             if peer is not None and recv is not None:
+                if self.staged:
+                    h = self._mirror(recv)
+                    back.append((recv, h))
+                    recv = h
                 ops.append(dist.P2POp(dist.irecv, recv, peer, self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        for dev, h in back:
+            dev.copy_(h)
 
 
 class LoopbackExchange:
