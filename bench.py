@@ -293,6 +293,10 @@ def run_reference_arm(args, rank, world):
 RANK_GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
 
 
+# configs whose per-GPU block is fixed as N grows (the others split one domain)
+WEAK_CONFIGS = ("c2", "weak", "c5w")
+
+
 def rank_grid(world):
     if world in RANK_GRIDS:
         return RANK_GRIDS[world]
@@ -402,7 +406,8 @@ def run_ours_multi(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if cfg_name in WEAK_CONFIGS else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE config initial conditions, g=0)",
         "config": {"workload": cfg["workload"], "nx": nx, "ny": ny, "nv1": 32, "nv2": 32,
                    "dt": dt, "parallelism": f"dd{px}x{py}",
