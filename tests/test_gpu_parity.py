@@ -277,3 +277,26 @@ def test_block_grid_steady_tracking(mm):
     assert np.isfinite(smax) and smax > 0.0 and secs > 0.0
     _, _, snan, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, 1e-3, 2, grid=(2, 2))
     assert np.isnan(snan)
+
+
+@pytest.mark.parametrize("shape", [(1, 7), (7, 1), (2, 2), (1, 1), (3, 50)])
+@pytest.mark.parametrize("faces_kind", ["periodic", "walls", "extrapolate"])
+def test_v1024_degenerate_grids_vs_oracle(mm, oracle, shape, faces_kind):
+    """The 32 x 32 kernel on degenerate spatial grids (a single column or
+    row, one cell, a band shorter than ly, ly + 2 rows): each cell's own
+    neighbour is itself under wrap, walls meet at corners.  10 steps."""
+    from paper_2509_21832_b200 import EXTRAPOLATE, PERIODIC, WallSpec
+    faces = {"periodic": (PERIODIC,) * 4, "extrapolate": (EXTRAPOLATE,) * 4,
+             "walls": (WallSpec(1.0), WallSpec(0.9), WallSpec(1.1), WallSpec(1.0, 0.2))}[faces_kind]
+    nx, ny = shape
+    mesh, bc, eps, model, Q, G, dt = _random_problem(mm, nx, ny, 32, faces, -0.5, 0.05, 11)
+    prob = oracle.Problem2D(mesh, bc, eps, model)
+    st = mm.State2D(0.0, Q, G)
+    Qo, Go = Q, G
+    for n in range(1, 11):
+        st = mm.step_2d(st, mesh, bc, eps, model, dt)
+        Qo, Go, _ = oracle.step_2d_arrays(prob, Qo, Go, dt)
+    assert q_rel_err(st.Q, Qo) <= TOL_N
+    # a lone periodic cell relaxes G to ~1e-6, pure roundoff of the O(0.1)
+    # Maxwellian terms (SURVEY 8c): compare G on a 1e-4 floor
+    assert rel_err(st.G, Go, floor=1e-4) <= TOL_G
