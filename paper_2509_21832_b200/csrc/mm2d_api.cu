@@ -430,16 +430,13 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     mc.qsrc = qsrc; mc.err = ctx->d_err; mc.dt = dt; mc.eps = c.eps; mc.nu = c.nu;
     mc.rx = dt / g.dx; mc.ry = dt / g.dy; mc.tau_kind = c.tau_kind; mc.tau_value = c.tau_value;
     mc.step = 0;
+    mc.Hout = H;
     k_macro_x<<<grid_for((long long)g.bx * (g.by + 2), 128), 128, 0, s>>>(mc);
     MARK(5);
     k_macro_y<<<grid_for((long long)g.bx * g.by, 128), 128, 0, s>>>(mc);
     MARK(6);
     nl += 3;
-    if (H) {
-        k_h_soa<<<grid_for((long long)g.bx * g.by, 256), 256, 0, s>>>(g, ctx->d_Hr, H);
-        ++nl;
-    }
-    MARK(7);
+    MARK(7);   // (the SoA heat output is written by k_macro_y)
     }   // phase 1: heat ring, macro
 #undef MARK
     CK(cudaGetLastError());

@@ -23,6 +23,7 @@ struct MacroArgs {
     const double* Qr;       // ring Q^n
     const double* Hr;       // ring heat tensor (AoS)
     double* Qx;             // ring Q** (x-swept)
+    double* Hout;           // (4, bx, by) heat tensor output (SoA) or null
     double* Qout;           // (bx, by, 6)
     const double* qsrc;     // (bx, by, 6) or null
     unsigned long long* err;
@@ -228,6 +229,11 @@ __global__ void k_macro_y(MacroArgs a) {
             const double* s = a.qsrc + 6 * ((size_t)i * g.by + j);
 #pragma unroll
             for (int m = 0; m < 6; ++m) q3[m] = q3[m] + a.dt * s[m];
+        }
+        // the step's heat tensor, SoA (4, bx, by) (macro2d.py:23-29)
+        if (a.Hout) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) a.Hout[(size_t)c * n + t] = hc[c];
         }
         double* qo = a.Qout + 6 * ((size_t)i * g.by + j);
         const int bs3 = bad_state(q3);
