@@ -43,13 +43,22 @@ constexpr int NT = 128;              // threads of the default 8-node (NP = 4) v
 constexpr int NP = 4;                // node pairs per thread (default variant)
 constexpr int TSLOTS = 4;            // table slots (rows j..j+3; the slot rebuilt
                                      // at iteration j last held row j-1)
-constexpr int KT = 0;                // K-table [32][8]
-constexpr int LT = KT + 8 * NV;      // L-table [8][32]
+constexpr int KW = 12;               // K-table entries per k
+constexpr int KT = 0;                // K-table [32][KW]
+constexpr int LT = KT + KW * NV;     // L-table [8][32]
 constexpr int GK = LT + 8 * NV;      // Gaussian k-table [32][2] (GA, GD)
-constexpr int GL = GK + 2 * NV;      // Gaussian l-table [2][32] (GB, GR)
-constexpr int TAB = GL + 2 * NV;     // 640 doubles per cell
-enum { K_W1N, K_H1, K_PE1, K_W1, K_U, K_C, K_Q1, K_P1 };   // pairs: (w1,h1) (pE1,W1) (U,c) (q1,p1)
-enum { L_E2, L_W2N, L_H2, L_W2, L_V, L_Q2, L_P2 };
+constexpr int GL = GK + 2 * NV;      // Gaussian l-table [32] (GB)
+constexpr int XT = GL + NV;          // Gaussian cross-term table [16][6] per even l
+constexpr int TAB = XT + 6 * 16;     // 832 doubles per cell
+// K-table pairs (16-byte loads): (w1, h1) (pE1, W1) (cx w1, cx h1) (W1^2, W1^3)
+// (pE1 U', pE1 c') (pE1 q1', pE1 p1') -- the target's k factors pre-multiplied
+// by the Maxwellian's k factor, the x-sum weights by the upwind coefficient
+enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_W12, K_W13, K_PU, K_PC, K_PQ1, K_PP1 };
+// L-table rows: E2, w2, h2, W2 and the target's l factors times E2
+enum { L_E2, L_W2N, L_H2, L_W2, L_EV, L_EW2, L_EP2, L_EQ2 };
+// cross-term table per even l = 2 lp: X0 = exp(q12 W1_0 W2), R = exp(q12 dv1 W2),
+// R^2, R^4, R^8 (the thread's base node k = kb gets X0 R^kb, its next pairs R^8)
+enum { X_X0, X_R1, X_R2, X_R4, X_R8 };
 
 inline size_t smem_bytes() {
     return sizeof(double) * (3 * V + TSLOTS * TAB + 4 * 16 + 16 + 2 * NV);
@@ -214,32 +223,38 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
 }
 
 // build the per-cell tables from the shared copy P of the cell's CellPar.
-// Work split so every warp does the same number of exps: warp 0 the K-table
-// (+ GD), warp 1 the L-table (+ GR), warps 2/3 the Gaussian GA / GB.
-// The closed-form target polynomial is stored pre-scaled by mtw = -wh/tau
-// with the Gaussian's -M wh/eps folded into U, so the node evaluates
-// acc = M (U' + V' + c' W2 + q1' p2 + p1' q2) (+ the Gaussian) directly.
+// Warp 0 the K-table, warp 1 the L-table and the cross-term table, warp 2
+// the Gaussian GA / GD, warp 3 GB.  The closed-form target polynomial is
+// stored pre-scaled by mtw = -wh/tau with the Gaussian's -M wh/eps folded
+// into U, and its k and l factors pre-multiplied by the Maxwellian's, so the
+// node evaluates acc = (pU) E2 + pE1 (E2 V') + (pc) (E2 W2) + (pq1) (E2 p2)
+// + (pp1) (E2 q2) (+ the Gaussian) with one product and four FMAs.
 template <int KS>
 __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, const CellPar& P,
                                              const double* v1s, const double* v2s, bool gauss,
                                              const double* etab) {
     const double mtw = -P.invtau * P.wh;
-    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
+    const int t = threadIdx.x;
     const int m = t & 31;
     if (t < 32) {
         const double W1 = v1s[m] - P.u1;
         const double W1s = W1 * W1;
         const double w1 = W1 * P.isT;
+        const double h1 = 0.5 * w1 * w1 - 1.0;
         const double q1 = W1s * P.inv2T - 2.0;
         const double p1 = W1 * P.gT1 * P.invT;
         const double U = W1s * P.s11 * P.inv2T + q1 * p1;
-        double* K = T + KT + 8 * m;
-        sts2(K + K_W1N, w1, 0.5 * w1 * w1 - 1.0);
-        sts2(K + K_PE1, P.pref * fexp(-W1s * P.inv2T, etab), W1);
-        sts2(K + K_U, fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
-             mtw * (2.0 * W1 * P.s12 * P.inv2T));
-        sts2(K + K_Q1, mtw * q1, mtw * p1);
-        if (gauss) T[GK + 2 * m + 1] = fexp(P.gq12 * W1 * (v2s[1] - v2s[0]), etab);
+        const double pe = P.pref * fexp(-W1s * P.inv2T, etab);
+        // the x-stage upwind coefficient (sign folded: v1 < 0 exactly for k < 16)
+        const double cxm = (m < NV / 2 ? -a.dt : a.dt) * v1s[m] * a.idx;
+        double* K = T + KT + KW * m;
+        sts2(K + K_W1N, w1, h1);
+        sts2(K + K_PE1, pe, W1);
+        sts2(K + K_XW, cxm * w1, cxm * h1);
+        sts2(K + K_W12, W1s, W1s * W1);
+        sts2(K + K_PU, pe * fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
+             pe * (mtw * (2.0 * W1 * P.s12 * P.inv2T)));
+        sts2(K + K_PQ1, pe * (mtw * q1), pe * (mtw * p1));
         if (m == 0) {
             sts2(T + HD + H_SCALE, P.scale, P.wg);
             sts2(T + HD + H_MTW, mtw, a.inveps * P.wh);
@@ -251,22 +266,39 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         const double w2 = W2 * P.isT;
         const double q2 = W2s * P.inv2T;
         const double p2 = W2 * P.gT2 * P.invT;
+        const double E2 = fexp(-W2s * P.inv2T, etab);
         double* L = T + LT + m;
-        L[L_E2 * NV] = fexp(-W2s * P.inv2T, etab);
+        L[L_E2 * NV] = E2;
         L[L_W2N * NV] = w2;
         L[L_H2 * NV] = 0.5 * w2 * w2;
         L[L_W2 * NV] = W2;
-        L[L_V * NV] = mtw * (q2 * p2 - W2s * P.s11 * P.inv2T);
-        L[L_Q2 * NV] = q2;
-        L[L_P2 * NV] = p2;
-        if (gauss) T[GL + NV + m] = fexp(P.gq12 * (v1s[KS] - v1s[0]) * W2, etab);
+        L[L_EV * NV] = E2 * (mtw * (q2 * p2 - W2s * P.s11 * P.inv2T));
+        L[L_EW2 * NV] = E2 * W2;
+        L[L_EP2 * NV] = E2 * p2;
+        L[L_EQ2 * NV] = E2 * q2;
+        if (gauss) {
+            // lanes 0-15: X0 at l = 2m; lanes 16-31: R and its powers at l = 2(m-16)
+            const int lp = m & 15;
+            const double W2e = v2s[2 * lp] - P.u2;
+            const double x = fexp(P.gq12 * (m < 16 ? v1s[0] - P.u1 : v1s[1] - v1s[0]) * W2e, etab);
+            double* X = T + XT + 6 * lp;
+            if (m < 16) {
+                X[X_X0] = x;
+            } else {
+                const double r2 = x * x, r4 = r2 * r2;
+                X[X_R1] = x;
+                X[X_R2] = r2;
+                X[X_R4] = r4;
+                X[X_R8] = r4 * r4;
+            }
+        }
     } else if (gauss && t < 96) {
         const double W1 = v1s[m] - P.u1;
-        T[GK + 2 * m] = P.gpref * a.inveps * P.wh * fexp(P.gq11 * (W1 * W1), etab);
+        sts2(T + GK + 2 * m, P.gpref * a.inveps * P.wh * fexp(P.gq11 * (W1 * W1), etab),
+             fexp(P.gq12 * W1 * (v2s[1] - v2s[0]), etab));
     } else if (gauss) {
         const double W2 = v2s[m] - P.u2;
         T[GL + m] = fexp(P.gq22 * (W2 * W2), etab);
-    }
     }
 }
 
@@ -404,9 +436,9 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     // node-pair offsets: off(p) = off0 + 256 p into a cell's block,
     // koff(p) = koff0 + 64 p into the K-table (immediate offsets in SASS)
     const int off0 = 32 * kb + lb;
-    const int koff0 = KT + 8 * kb;
+    const int koff0 = KT + KW * kb;
 #define off_(p) (off0 + 32 * KS * (p))
-#define koff_(p) (koff0 + 8 * KS * (p))
+#define koff_(p) (koff0 + KW * KS * (p))
     double cx[NP_];
 #pragma unroll
     for (int p = 0; p < NP_; ++p)
@@ -414,6 +446,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     const bool negy = v2s[lb] < 0.0;
     const double sy = negy ? -a.dt : a.dt;
     const double cy0 = sy * v2s[lb] * a.idy, cy1 = sy * v2s[lb + 1] * a.idy;
+    const int xsel = lp * 6;       // this thread's cross-term table row
     const size_t V_ = V;
 
     const int i = blockIdx.x;
@@ -526,31 +559,11 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
 #pragma unroll
     for (int q = 0; q < 2 * NP_; ++q) ty[q] = 0.0;
 
-    // one transport stage's four projection sums from the thread's pairs
-    auto stage_sums = [&](const double* T, const double (&y)[2 * NP_], double* s) {
-        const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
-        const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
-        double Y0 = y[0], Y1 = y[1], S1, S3;
-        {
-            const double2 wh = lds2(T + koff_(0) + K_W1N);   // w1, h1
-            const double ys = y[0] + y[1];
-            S1 = wh.x * ys;
-            S3 = wh.y * ys;
-        }
-#pragma unroll
-        for (int p = 1; p < NP_; ++p) {
-            const double2 wh = lds2(T + koff_(p) + K_W1N);
-            const double ys = y[2 * p] + y[2 * p + 1];
-            Y0 += y[2 * p];
-            Y1 += y[2 * p + 1];
-            S1 = fma(wh.x, ys, S1);
-            S3 = fma(wh.y, ys, S3);
-        }
-        s[0] = Y0 + Y1;
-        s[1] = S1;
-        s[2] = fma(w2.x, Y0, w2.y * Y1);
-        s[3] = S3 + fma(h2.x, Y0, h2.y * Y1);
-    };
+    // Transport stages work on the upwind differences d = G_self - G_upwind:
+    // the stage output is G - c d (one FMA) and the four projection sums of
+    // Y = c d are formed from d with the coefficient folded into the weights.
+    // x-stage: c depends on k only, so the K-table carries (c w1, c h1).
+    // y-stage: c depends on l only (cy0, cy1), applied once per thread.
 
     auto body = [&](int j, auto steady) {
         constexpr bool ST = decltype(steady)::value;
@@ -602,34 +615,63 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         double s[12];
 #pragma unroll
         for (int q = 0; q < 8; ++q) s[q] = 0.0;
-        // 2. y-sums of row j: Y = cy (G*_j - G*_upwind)
+        // 2. y-stage of row j: d = G*_j - G*_upwind, G** - dt Zhat = G*_j - cy d
         if (row_j) {
             if (!ST) tm_wait_st();         // the bottom-ghost copy may have just written R1
-            double c[2 * NP_], y[2 * NP_];
+            double c[2 * NP_];
             tm_ld8(R1, c);
             if (!negy) tm_ld8(R0, gst);     // warp-uniform; v2 < 0 warps use G*(j+1) = gst
+            const double2 w2 = lds2(T0 + LT + L_W2N * NV + lb);
+            const double2 h2 = lds2(T0 + LT + L_H2 * NV + lb);
+            double D0, D1, S1, S3;
 #pragma unroll
-            for (int q = 0; q < 2 * NP_; ++q) {
-                y[q] = ((q & 1) ? cy1 : cy0) * (c[q] - gst[q]);
-                ty[q] = c[q] - y[q];
+            for (int p = 0; p < NP_; ++p) {
+                const double d0 = c[2 * p] - gst[2 * p], d1 = c[2 * p + 1] - gst[2 * p + 1];
+                ty[2 * p] = fma(-cy0, d0, c[2 * p]);
+                ty[2 * p + 1] = fma(-cy1, d1, c[2 * p + 1]);
+                const double e = fma(cy0, d0, cy1 * d1);
+                const double2 wh = lds2(T0 + koff_(p) + K_W1N);   // w1, h1
+                if (p == 0) {
+                    D0 = d0; D1 = d1; S1 = wh.x * e; S3 = wh.y * e;
+                } else {
+                    D0 += d0; D1 += d1; S1 = fma(wh.x, e, S1); S3 = fma(wh.y, e, S3);
+                }
             }
-            stage_sums(T0, y, s);
+            const double Y0 = cy0 * D0, Y1 = cy1 * D1;
+            s[0] = Y0 + Y1;
+            s[1] = S1;
+            s[2] = fma(w2.x, Y0, w2.y * Y1);
+            s[3] = S3 + fma(h2.x, Y0, h2.y * Y1);
         }
-        // 3. x-stage of row j+2 into the slot of row j-1: G - dt Z_x
+        // 3. x-stage of row j+2 into the slot of row j-1: G - dt Z_x = G - cx d
         const bool do_x = ST || computes(rx);
         if (do_x) {
             mbar_wait(mbar, (nload - 1) & 1);   // this row's bulk loads (issued one iteration ago)
-            double y[2 * NP_], xs[2 * NP_];
+            const double* T = T2;
+            const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
+            const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
+            double xs[2 * NP_];
+            double Y0, Y1, S1, S3;
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
                 const double2 c = lds2(stg + off_(p)), h = lds2(stg + V + off_(p));
-                y[2 * p] = cx[p] * (c.x - h.x);
-                y[2 * p + 1] = cx[p] * (c.y - h.y);
-                xs[2 * p] = c.x - y[2 * p];
-                xs[2 * p + 1] = c.y - y[2 * p + 1];
+                const double d0 = c.x - h.x, d1 = c.y - h.y;
+                xs[2 * p] = fma(-cx[p], d0, c.x);
+                xs[2 * p + 1] = fma(-cx[p], d1, c.y);
+                const double e = d0 + d1;
+                const double2 xw = lds2(T + koff_(p) + K_XW);      // cx w1, cx h1
+                if (p == 0) {
+                    Y0 = cx[p] * d0; Y1 = cx[p] * d1; S1 = xw.x * e; S3 = xw.y * e;
+                } else {
+                    Y0 = fma(cx[p], d0, Y0); Y1 = fma(cx[p], d1, Y1);
+                    S1 = fma(xw.x, e, S1); S3 = fma(xw.y, e, S3);
+                }
             }
             tm_st8(R0, xs);
-            stage_sums(T2, y, s + 4);
+            s[4] = Y0 + Y1;
+            s[5] = S1;
+            s[6] = fma(w2.x, Y0, w2.y * Y1);
+            s[7] = S3 + fma(h2.x, Y0, h2.y * Y1);
         }
         s[8] = hs[0]; s[9] = hs[1]; s[10] = hs[2]; s[11] = hs[3];
         // 4. the row's block reduction; the CellPar staged one iteration
@@ -650,21 +692,29 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         double acc[2 * NP_];
         const double* wsrc = wx ? wx + (size_t)j * V_
                                 : (ST ? nullptr : (j == 0 ? wb : (j == g.by - 1 ? wt : nullptr)));
+        // acc = wh g^ + wg (G* - dt Z_y): everything of G^{n+1}(j) but the
+        // y-projection, which waits for this reduction
         if (row_j) {
             const double* T = T0;
-            const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
-            const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
+            const double wg = T[HD + H_WG];
             if (wsrc == nullptr) {
-                const double2 Vl = lds2(T + LT + L_V * NV + lb);
-                const double2 q2 = lds2(T + LT + L_Q2 * NV + lb);
-                const double2 p2 = lds2(T + LT + L_P2 * NV + lb);
-                // ES-BGK Gaussian: X(k, l) = exp(c12 W1 W2 / det), by recurrence
+                const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
+                const double2 eV = lds2(T + LT + L_EV * NV + lb);
+                const double2 eW = lds2(T + LT + L_EW2 * NV + lb);
+                const double2 ep = lds2(T + LT + L_EP2 * NV + lb);
+                const double2 eq = lds2(T + LT + L_EQ2 * NV + lb);
+                // ES-BGK Gaussian GA GB X with X(k, l) = exp(q12 W1 W2): the
+                // thread's base X0 R^kb from the cross-term table, then R^8 per pair
                 double2 GB = make_double2(0.0, 0.0);
                 double GR = 1.0, Xp = 0.0;
                 if (gauss) {
                     GB = lds2(T + GL + lb);
-                    GR = T[GL + NV + lb];
-                    Xp = fexp(T[HD + H_GQ12] * T[KT + 8 * kb + K_W1] * W2.x, etab);
+                    const double2 x0 = lds2(T + XT + xsel + X_X0);   // X0, R
+                    const double2 r24 = lds2(T + XT + xsel + X_R2);  // R^2, R^4
+                    GR = T[XT + xsel + X_R8];
+                    Xp = x0.x * ((kb & 1) ? x0.y : 1.0);
+                    Xp *= (kb & 2) ? r24.x : 1.0;
+                    Xp *= (kb & 4) ? r24.y : 1.0;
                 }
 #pragma unroll
                 for (int p = 0; p < NP_; ++p) {
@@ -672,22 +722,24 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                     const double pe = K[K_PE1];
                     // closed-form target (_core.pyx:220-224), factored and
                     // pre-scaled by -wh/tau (minus wh/eps when Gaussian)
-                    const double2 Uc = lds2(K + K_U);   // U', c'
-                    const double2 qp = lds2(K + K_Q1);  // q1', p1'
-                    double P0 = Uc.x + Vl.x, P1 = Uc.x + Vl.y;
-                    P0 = fma(Uc.y, W2.x, P0); P1 = fma(Uc.y, W2.y, P1);
-                    P0 = fma(qp.x, p2.x, P0); P1 = fma(qp.x, p2.y, P1);
-                    P0 = fma(qp.y, q2.x, P0); P1 = fma(qp.y, q2.y, P1);
-                    acc[2 * p] = P0 * (pe * E2.x);
-                    acc[2 * p + 1] = P1 * (pe * E2.y);
+                    const double2 pu = lds2(K + K_PU);   // pe U', pe c'
+                    const double2 pq = lds2(K + K_PQ1);  // pe q1', pe p1'
+                    double P0 = fma(wg, ty[2 * p], pu.x * E2.x);
+                    double P1 = fma(wg, ty[2 * p + 1], pu.x * E2.y);
+                    P0 = fma(pe, eV.x, P0); P1 = fma(pe, eV.y, P1);
+                    P0 = fma(pu.y, eW.x, P0); P1 = fma(pu.y, eW.y, P1);
+                    P0 = fma(pq.x, ep.x, P0); P1 = fma(pq.x, ep.y, P1);
+                    P0 = fma(pq.y, eq.x, P0); P1 = fma(pq.y, eq.y, P1);
                     if (gauss) {
                         // + Gaussian wh/eps, Gaussian = GA GB X
                         const double2 gad = lds2(T + GK + 2 * (kb + KS * p));   // GA', GD
                         const double Y0 = gad.x * Xp;
-                        acc[2 * p] = fma(GB.x, Y0, acc[2 * p]);
-                        acc[2 * p + 1] = fma(GB.y, Y0 * gad.y, acc[2 * p + 1]);
+                        P0 = fma(GB.x, Y0, P0);
+                        P1 = fma(GB.y, Y0 * gad.y, P1);
                         Xp *= GR;
                     }
+                    acc[2 * p] = P0;
+                    acc[2 * p + 1] = P1;
                 }
             } else {
                 // wall-strip target (boundary.py:343-378), precomputed
@@ -695,8 +747,8 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
 #pragma unroll
                 for (int p = 0; p < NP_; ++p) {
                     const double2 w = __ldg(reinterpret_cast<const double2*>(wsrc + off_(p)));
-                    acc[2 * p] = wh_ * w.x;
-                    acc[2 * p + 1] = wh_ * w.y;
+                    acc[2 * p] = fma(wg, ty[2 * p], wh_ * w.x);
+                    acc[2 * p + 1] = fma(wg, ty[2 * p + 1], wh_ * w.y);
                 }
             }
         }
@@ -709,34 +761,41 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         // 5. G**(j), relax, store, heat partials
         hs[0] = hs[1] = hs[2] = hs[3] = 0.0;
         if (row_j) {
+            // G^{n+1} = acc + wg Zhat_y, Zhat_y = (a1 + w1 a2 + h1 a4 + w2 a3 + h2 a4) M
+            // split as (al pE1) E2 + pE1 (b E2) with wg folded into the a's
             const double* T = T0;
-            const double sc = T[HD + H_SCALE];
+            const double sc = T[HD + H_SCALE] * T[HD + H_WG];
             const double a1 = s[0] * sc, a2 = s[1] * sc, a3 = s[2] * sc, a4 = s[3] * sc;
-            const double wg = T[HD + H_WG];
             const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
             const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
-            const double b0 = fma(w2.x, a3, h2.x * a4), b1 = fma(w2.y, a3, h2.y * a4);
+            const double bE0 = fma(w2.x, a3, h2.x * a4) * E2.x;
+            const double bE1 = fma(w2.y, a3, h2.y * a4) * E2.y;
             double* out = out_b + (size_t)j * V_;
-            double A0x = 0, A0y = 0, A1x = 0, A1y = 0, A2x = 0, A2y = 0, A3x = 0, A3y = 0;
+            double A0x, A0y, A1x, A1y, A2x, A2y, A3x, A3y;
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
                 const double* K = T + koff_(p);
                 const double2 wh = lds2(K + K_W1N);     // w1, h1
                 const double2 pw = lds2(K + K_PE1);     // pE1, W1
-                const double al = fma(wh.x, a2, fma(wh.y, a4, a1));
-                const double M0 = pw.x * E2.x, M1 = pw.x * E2.y;
-                const double gs0 = fma(al + b0, M0, ty[2 * p]);
-                const double gs1 = fma(al + b1, M1, ty[2 * p + 1]);
-                const double o0 = fma(wg, gs0, acc[2 * p]), o1 = fma(wg, gs1, acc[2 * p + 1]);
+                const double2 w3 = lds2(K + K_W12);     // W1^2, W1^3
+                const double alp = fma(wh.x, a2, fma(wh.y, a4, a1)) * pw.x;
+                const double o0 = fma(alp, E2.x, fma(bE0, pw.x, acc[2 * p]));
+                const double o1 = fma(alp, E2.y, fma(bE1, pw.x, acc[2 * p + 1]));
                 *reinterpret_cast<double2*>(out + off_(p)) = make_double2(o0, o1);
                 // heat moments about u^n (_core.pyx:303-321): A_a = sum W1^a o
-                const double W1 = pw.y, W11 = W1 * W1, W111 = W11 * W1;
-                A0x += o0; A0y += o1;
-                A1x = fma(W1, o0, A1x); A1y = fma(W1, o1, A1y);
-                A2x = fma(W11, o0, A2x); A2y = fma(W11, o1, A2y);
-                A3x = fma(W111, o0, A3x); A3y = fma(W111, o1, A3y);
+                if (p == 0) {
+                    A0x = o0; A0y = o1;
+                    A1x = pw.y * o0; A1y = pw.y * o1;
+                    A2x = w3.x * o0; A2y = w3.x * o1;
+                    A3x = w3.y * o0; A3y = w3.y * o1;
+                } else {
+                    A0x += o0; A0y += o1;
+                    A1x = fma(pw.y, o0, A1x); A1y = fma(pw.y, o1, A1y);
+                    A2x = fma(w3.x, o0, A2x); A2y = fma(w3.x, o1, A2y);
+                    A3x = fma(w3.y, o0, A3x); A3y = fma(w3.y, o1, A3y);
+                }
             }
             const double W2xx = W2.x * W2.x, W2yy = W2.y * W2.y;
             hs[0] = A3x + A3y;
