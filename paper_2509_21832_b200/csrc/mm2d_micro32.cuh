@@ -48,8 +48,8 @@ constexpr int KT = 0;                // K-table [32][KW]
 constexpr int LT = KT + KW * NV;     // L-table [8][32]
 constexpr int GK = LT + 8 * NV;      // Gaussian k-table [32][2] (GA, GD)
 constexpr int GL = GK + 2 * NV;      // Gaussian l-table [32] (GB)
-constexpr int XT = GL + NV;          // Gaussian cross-term table [16][6] per even l
-constexpr int TAB = XT + 6 * 16;     // 832 doubles per cell
+constexpr int XT = GL + NV;          // Gaussian cross-term table [16][4] per even l + R^8 [16]
+constexpr int TAB = XT + 5 * 16;     // 816 doubles per cell
 // K-table pairs (16-byte loads): (w1, h1) (pE1, W1) (cx w1, cx h1) (W1^2, W1^3)
 // (pE1 U', pE1 c') (pE1 q1', pE1 p1') -- the target's k factors pre-multiplied
 // by the Maxwellian's k factor, the x-sum weights by the upwind coefficient
@@ -58,7 +58,7 @@ enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_W12, K_W13, K_PU, K_PC, K_PQ1, K_
 enum { L_E2, L_W2N, L_H2, L_W2, L_EV, L_EW2, L_EP2, L_EQ2 };
 // cross-term table per even l = 2 lp: X0 = exp(q12 W1_0 W2), R = exp(q12 dv1 W2),
 // R^2, R^4, R^8 (the thread's base node k = kb gets X0 R^kb, its next pairs R^8)
-enum { X_X0, X_R1, X_R2, X_R4, X_R8 };
+enum { X_X0, X_R1, X_R2, X_R4, X_R8 = 4 * 16 };   // X_R8: offset of the R^8 row
 
 inline size_t smem_bytes() {
     return sizeof(double) * (3 * V + TSLOTS * TAB + 4 * 16 + 16 + 2 * NV);
@@ -281,7 +281,7 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
             const int lp = m & 15;
             const double W2e = v2s[2 * lp] - P.u2;
             const double x = fexp(P.gq12 * (m < 16 ? v1s[0] - P.u1 : v1s[1] - v1s[0]) * W2e, etab);
-            double* X = T + XT + 6 * lp;
+            double* X = T + XT + 4 * lp;
             if (m < 16) {
                 X[X_X0] = x;
             } else {
@@ -289,7 +289,7 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
                 X[X_R1] = x;
                 X[X_R2] = r2;
                 X[X_R4] = r4;
-                X[X_R8] = r4 * r4;
+                T[XT + X_R8 + lp] = r4 * r4;
             }
         }
     } else if (gauss && t < 96) {
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     const bool negy = v2s[lb] < 0.0;
     const double sy = negy ? -a.dt : a.dt;
     const double cy0 = sy * v2s[lb] * a.idy, cy1 = sy * v2s[lb + 1] * a.idy;
-    const int xsel = lp * 6;       // this thread's cross-term table row
+    const int xsel = lp * 4;       // this thread's cross-term table row
     const size_t V_ = V;
 
     const int i = blockIdx.x;
@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                     GB = lds2(T + GL + lb);
                     const double2 x0 = lds2(T + XT + xsel + X_X0);   // X0, R
                     const double2 r24 = lds2(T + XT + xsel + X_R2);  // R^2, R^4
-                    GR = T[XT + xsel + X_R8];
+                    GR = T[XT + X_R8 + lp];
                     Xp = x0.x * ((kb & 1) ? x0.y : 1.0);
                     Xp *= (kb & 2) ? r24.x : 1.0;
                     Xp *= (kb & 4) ? r24.y : 1.0;
