@@ -345,7 +345,15 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // access pattern of the thread-private G* ring: 8 doubles of a thread's row
 // are 16 consecutive 32-bit columns of its lane, moved by ONE
 // tcgen05.ld/st .32x32b.x16 (against four 16-byte LDS/STS in shared memory).
-__device__ __forceinline__ void tm_st8(unsigned addr, const double (&v)[8]) {
+#ifndef TM_SPLIT
+#define TM_SPLIT 1   // tcgen05 ld/st instructions per 8-double row (1: .x16, 2: .x8, 4: .x4)
+#endif
+template <int N>   // N doubles = 2N columns
+__device__ __forceinline__ void tm_st_n(unsigned addr, const double* v);
+template <int N>
+__device__ __forceinline__ void tm_ld_n(unsigned addr, double* v);
+template <>
+__device__ __forceinline__ void tm_st_n<8>(unsigned addr, const double* v) {
     // the doubles are split inside PTX so ptxas can place them straight into
     // the 16 consecutive registers STTM reads
     asm volatile(
@@ -358,7 +366,27 @@ __device__ __forceinline__ void tm_st8(unsigned addr, const double (&v)[8]) {
         "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]), "d"(v[4]), "d"(v[5]), "d"(v[6]), "d"(v[7])
         : "memory");
 }
-__device__ __forceinline__ void tm_ld8(unsigned addr, double (&v)[8]) {
+template <>
+__device__ __forceinline__ void tm_st_n<4>(unsigned addr, const double* v) {
+    asm volatile(
+        "{\n .reg .b32 a<8>;\n"
+        " mov.b64 {a0, a1}, %1;\n mov.b64 {a2, a3}, %2;\n mov.b64 {a4, a5}, %3;\n"
+        " mov.b64 {a6, a7}, %4;\n"
+        " tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {a0, a1, a2, a3, a4, a5, a6, a7};\n}\n" ::"r"(addr),
+        "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+        : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_st_n<2>(unsigned addr, const double* v) {
+    asm volatile(
+        "{\n .reg .b32 a<4>;\n"
+        " mov.b64 {a0, a1}, %1;\n mov.b64 {a2, a3}, %2;\n"
+        " tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {a0, a1, a2, a3};\n}\n" ::"r"(addr),
+        "d"(v[0]), "d"(v[1])
+        : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld_n<8>(unsigned addr, double* v) {
     asm volatile(
         "{\n .reg .b32 a<16>;\n"
         " tcgen05.ld.sync.aligned.32x32b.x16.b32 {a0, a1, a2, a3, a4, a5, a6, a7, a8, a9, a10, "
@@ -371,6 +399,42 @@ __device__ __forceinline__ void tm_ld8(unsigned addr, double (&v)[8]) {
           "=d"(v[7])
         : "r"(addr)
         : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld_n<4>(unsigned addr, double* v) {
+    asm volatile(
+        "{\n .reg .b32 a<8>;\n"
+        " tcgen05.ld.sync.aligned.32x32b.x8.b32 {a0, a1, a2, a3, a4, a5, a6, a7}, [%4];\n"
+        " mov.b64 %0, {a0, a1};\n mov.b64 %1, {a2, a3};\n mov.b64 %2, {a4, a5};\n"
+        " mov.b64 %3, {a6, a7};\n}\n"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+        : "r"(addr)
+        : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_ld_n<2>(unsigned addr, double* v) {
+    asm volatile(
+        "{\n .reg .b32 a<4>;\n"
+        " tcgen05.ld.sync.aligned.32x32b.x4.b32 {a0, a1, a2, a3}, [%2];\n"
+        " mov.b64 %0, {a0, a1};\n mov.b64 %1, {a2, a3};\n}\n"
+        : "=d"(v[0]), "=d"(v[1])
+        : "r"(addr)
+        : "memory");
+}
+__device__ __forceinline__ void tm_st8(unsigned addr, const double (&v)[8]) {
+    constexpr int N = 8 / TM_SPLIT;
+#pragma unroll
+    for (int q = 0; q < TM_SPLIT; ++q) tm_st_n<N>(addr + 2 * N * q, v + N * q);
+}
+__device__ __forceinline__ void tm_ld8(unsigned addr, double (&v)[8]) {
+    constexpr int N = 8 / TM_SPLIT;
+    if constexpr (TM_SPLIT == 1) {
+        tm_ld_n<8>(addr, v);
+    } else {
+#pragma unroll
+        for (int q = 0; q < TM_SPLIT; ++q) tm_ld_n<N>(addr + 2 * N * q, v + N * q);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    }
 }
 __device__ __forceinline__ void tm_wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
@@ -615,12 +679,15 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         double s[12];
 #pragma unroll
         for (int q = 0; q < 8; ++q) s[q] = 0.0;
-        // 2. y-stage of row j: d = G*_j - G*_upwind, G** - dt Zhat = G*_j - cy d
+        // 2. y-stage of row j: d = G*_j - G*_upwind, G** - dt Zhat = G*_j - cy d.
+        //    Both rows come back from the ring (the upwind row is j+1 for the
+        //    v2 < 0 warps, j-1 for the others; warp-uniform), so the recon
+        //    registers die at their store and no register copies are needed.
         if (row_j) {
-            if (!ST) tm_wait_st();         // the bottom-ghost copy may have just written R1
+            tm_wait_st();                  // G*(j+1) and any ghost copy are in the ring
             double c[2 * NP_];
             tm_ld8(R1, c);
-            if (!negy) tm_ld8(R0, gst);     // warp-uniform; v2 < 0 warps use G*(j+1) = gst
+            tm_ld8(negy ? R2 : R0, gst);
             const double2 w2 = lds2(T0 + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T0 + LT + L_H2 * NV + lb);
             double D0, D1, S1, S3;
