@@ -51,11 +51,12 @@ constexpr int GL = GK + 2 * NV;      // Gaussian l-table [32] (GB)
 constexpr int XT = GL + NV;          // Gaussian cross-term table [16][4] per even l + R^8 [16]
 constexpr int TAB = XT + 5 * 16;     // 816 doubles per cell
 // K-table pairs (16-byte loads): (w1, h1) (pE1, W1) (cx w1, cx h1) (W1^2, W1^3)
-// (pE1 U', pE1 c') (pE1 q1', pE1 p1') -- the target's k factors pre-multiplied
-// by the Maxwellian's k factor, the x-sum weights by the upwind coefficient
-enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_W12, K_W13, K_PU, K_PC, K_PQ1, K_PP1 };
-// L-table rows: E2, w2, h2, W2 and the target's l factors times E2
-enum { L_E2, L_W2N, L_H2, L_W2, L_EV, L_EW2, L_EP2, L_EQ2 };
+// (pE1 f0, pE1 f1) (pE1 f2, -) -- the target polynomial's W2-power
+// coefficients pre-multiplied by the Maxwellian's k factor, the x-sum weights
+// by the upwind coefficient
+enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_W12, K_W13, K_F0, K_F1, K_F2, K_F2PAD };
+// L-table rows: E2, w2, h2, W2, E2 W2, E2 W2^2, f3 E2 W2^3
+enum { L_E2, L_W2N, L_H2, L_W2, L_EW1, L_EW2, L_EW3, L_PAD };
 // cross-term table per even l = 2 lp: X0 = exp(q12 W1_0 W2), R = exp(q12 dv1 W2),
 // R^2, R^4, R^8 (the thread's base node k = kb gets X0 R^kb, its next pairs R^8)
 enum { X_X0, X_R1, X_R2, X_R4, X_R8 = 4 * 16 };   // X_R8: offset of the R^8 row
@@ -138,16 +139,25 @@ __constant__ double kExp2Tab[64] = {
     1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
     1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
 
+// the reduction and polynomial constants sit in the constant bank so every
+// step is one DFMA with a c[][] operand (64-bit literals would each cost a
+// pair of uniform-register moves)
+__constant__ double kExpC[7] = {92.33248261689366,          // 64 / ln 2
+                                -0.010830424696249145,      // ln2/64, high part
+                                -3.623510646634843e-19,     // ln2/64, low part
+                                1.3888888888888889e-03, 8.3333333333333333e-03,
+                                4.1666666666666667e-02, 1.6666666666666667e-01};
+
 __device__ __forceinline__ double fexp(double x, const double* etab) {
     const double SH = 6755399441055744.0;   // 1.5 * 2^52: round-to-int shifter
-    double t = fma(x, 92.33248261689366, SH);            // x 64 / ln 2
+    double t = fma(x, kExpC[0], SH);
     const int n = __double2loint(t);
     t -= SH;
-    double r = fma(t, -0.010830424696249145, x);         // ln2/64, high part
-    r = fma(t, -3.623510646634843e-19, r);               // ln2/64, low part
-    double p = fma(r, 1.3888888888888889e-03, 8.3333333333333333e-03);
-    p = fma(p, r, 4.1666666666666667e-02);
-    p = fma(p, r, 1.6666666666666667e-01);
+    double r = fma(t, kExpC[1], x);
+    r = fma(t, kExpC[2], r);
+    double p = fma(r, kExpC[3], kExpC[4]);
+    p = fma(p, r, kExpC[5]);
+    p = fma(p, r, kExpC[6]);
     p = fma(p, r, 0.5);
     p = fma(p, r, 1.0);
     const double q = p * r;                               // e^r - 1
@@ -226,9 +236,10 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
 // Warp 0 the K-table, warp 1 the L-table and the cross-term table, warp 2
 // the Gaussian GA / GD, warp 3 GB.  The closed-form target polynomial is
 // stored pre-scaled by mtw = -wh/tau with the Gaussian's -M wh/eps folded
-// into U, and its k and l factors pre-multiplied by the Maxwellian's, so the
-// node evaluates acc = (pU) E2 + pE1 (E2 V') + (pc) (E2 W2) + (pq1) (E2 p2)
-// + (pp1) (E2 q2) (+ the Gaussian) with one product and four FMAs.
+// into U.  As a polynomial in W2 the bracket is f0(k) + f1(k) W2 + f2(k) W2^2
+// + f3 W2^3 (f3 cell-constant), so with the Maxwellian's factors folded in the
+// node evaluates acc = (pE1 f0) E2 + (pE1 f1) (E2 W2) + (pE1 f2) (E2 W2^2)
+// + pE1 (f3 E2 W2^3) (+ the Gaussian) with one product and three FMAs.
 template <int KS>
 __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, const CellPar& P,
                                              const double* v1s, const double* v2s, bool gauss,
@@ -252,9 +263,11 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         sts2(K + K_PE1, pe, W1);
         sts2(K + K_XW, cxm * w1, cxm * h1);
         sts2(K + K_W12, W1s, W1s * W1);
-        sts2(K + K_PU, pe * fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
-             pe * (mtw * (2.0 * W1 * P.s12 * P.inv2T)));
-        sts2(K + K_PQ1, pe * (mtw * q1), pe * (mtw * p1));
+        // bracket U + V + c W2 + q1 p2 + p1 q2 (_core.pyx:220-224) by powers of W2:
+        // f0 = U, f1 = (W1 s12 + q1 gT2) / T, f2 = (p1 - s11) / (2T), f3 = gT2 / (2T^2)
+        sts2(K + K_F0, pe * fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
+             pe * (mtw * ((W1 * P.s12 + q1 * P.gT2) * P.invT)));
+        sts2(K + K_F2, pe * (mtw * ((p1 - P.s11) * P.inv2T)), 0.0);
         if (m == 0) {
             sts2(T + HD + H_SCALE, P.scale, P.wg);
             sts2(T + HD + H_MTW, mtw, a.inveps * P.wh);
@@ -264,18 +277,15 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         const double W2 = v2s[m] - P.u2;
         const double W2s = W2 * W2;
         const double w2 = W2 * P.isT;
-        const double q2 = W2s * P.inv2T;
-        const double p2 = W2 * P.gT2 * P.invT;
         const double E2 = fexp(-W2s * P.inv2T, etab);
         double* L = T + LT + m;
         L[L_E2 * NV] = E2;
         L[L_W2N * NV] = w2;
         L[L_H2 * NV] = 0.5 * w2 * w2;
         L[L_W2 * NV] = W2;
-        L[L_EV * NV] = E2 * (mtw * (q2 * p2 - W2s * P.s11 * P.inv2T));
-        L[L_EW2 * NV] = E2 * W2;
-        L[L_EP2 * NV] = E2 * p2;
-        L[L_EQ2 * NV] = E2 * q2;
+        L[L_EW1 * NV] = E2 * W2;
+        L[L_EW2 * NV] = E2 * W2s;
+        L[L_EW3 * NV] = (mtw * (P.gT2 * P.invT * P.inv2T)) * (E2 * (W2s * W2));
         if (gauss) {
             // lanes 0-15: X0 at l = 2m; lanes 16-31: R and its powers at l = 2(m-16)
             const int lp = m & 15;
@@ -766,10 +776,9 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             const double wg = T[HD + H_WG];
             if (wsrc == nullptr) {
                 const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
-                const double2 eV = lds2(T + LT + L_EV * NV + lb);
-                const double2 eW = lds2(T + LT + L_EW2 * NV + lb);
-                const double2 ep = lds2(T + LT + L_EP2 * NV + lb);
-                const double2 eq = lds2(T + LT + L_EQ2 * NV + lb);
+                const double2 e1 = lds2(T + LT + L_EW1 * NV + lb);
+                const double2 e2 = lds2(T + LT + L_EW2 * NV + lb);
+                const double2 e3 = lds2(T + LT + L_EW3 * NV + lb);
                 // ES-BGK Gaussian GA GB X with X(k, l) = exp(q12 W1 W2): the
                 // thread's base X0 R^kb from the cross-term table, then R^8 per pair
                 double2 GB = make_double2(0.0, 0.0);
@@ -789,14 +798,13 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                     const double pe = K[K_PE1];
                     // closed-form target (_core.pyx:220-224), factored and
                     // pre-scaled by -wh/tau (minus wh/eps when Gaussian)
-                    const double2 pu = lds2(K + K_PU);   // pe U', pe c'
-                    const double2 pq = lds2(K + K_PQ1);  // pe q1', pe p1'
-                    double P0 = fma(wg, ty[2 * p], pu.x * E2.x);
-                    double P1 = fma(wg, ty[2 * p + 1], pu.x * E2.y);
-                    P0 = fma(pe, eV.x, P0); P1 = fma(pe, eV.y, P1);
-                    P0 = fma(pu.y, eW.x, P0); P1 = fma(pu.y, eW.y, P1);
-                    P0 = fma(pq.x, ep.x, P0); P1 = fma(pq.x, ep.y, P1);
-                    P0 = fma(pq.y, eq.x, P0); P1 = fma(pq.y, eq.y, P1);
+                    const double2 f01 = lds2(K + K_F0);   // pe f0', pe f1'
+                    const double f2 = K[K_F2];             // pe f2'
+                    double P0 = fma(wg, ty[2 * p], f01.x * E2.x);
+                    double P1 = fma(wg, ty[2 * p + 1], f01.x * E2.y);
+                    P0 = fma(f01.y, e1.x, P0); P1 = fma(f01.y, e1.y, P1);
+                    P0 = fma(f2, e2.x, P0); P1 = fma(f2, e2.y, P1);
+                    P0 = fma(pe, e3.x, P0); P1 = fma(pe, e3.y, P1);
                     if (gauss) {
                         // + Gaussian wh/eps, Gaussian = GA GB X
                         const double2 gad = lds2(T + GK + 2 * (kb + KS * p));   // GA', GD
