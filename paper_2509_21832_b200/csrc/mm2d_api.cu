@@ -241,12 +241,12 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
         // Band height: a CTA walks one column through ly rows, paying ~4
         // pipeline-fill iterations per band.  Measured on C2 (256 x 256,
-        // 148 SMs x 3 CTAs): ly 36..60 gives 0.54-0.58 ms with a flat optimum
-        // at 48-56; a wave-quantisation model (pick ly minimising
-        // waves * (ly + 4)) predicted 52 and was not better, because the
-        // short last band of ly = 48 (16 rows) already fills the tail.
+        // 148 SMs x 3 CTAs, kernel v16): ly 48 / 50 / 52 / 54 / 56 / 58 / 60 / 64
+        // give 0.412 / 0.411 / 0.415 / 0.411 / 0.407 / 0.411 / 0.416 / 0.424 ms;
+        // a wave-quantisation model (minimise waves * (ly + 4)) predicts 52
+        // and is not borne out, so the measured optimum is the default.
         const char* ly = getenv("MM2D_LY");
-        ctx->ly32 = ly ? std::max(1, atoi(ly)) : 48;
+        ctx->ly32 = ly ? std::max(1, atoi(ly)) : 56;
         ctx->ly32 = std::min(ctx->ly32, g.by);
         const long long items = (long long)((g.by + ctx->ly32 - 1) / ctx->ly32) * g.bx;
         const char* pe = getenv("MM2D_PERSIST");
