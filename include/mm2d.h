@@ -51,6 +51,9 @@ extern "C" {
 #define MM2D_FACE_PERIODIC 0
 #define MM2D_FACE_EXTRAPOLATE 1
 #define MM2D_FACE_WALL 2
+/* specularly reflecting wall: extension, the reference has diffuse walls only
+   (mirror ghosts in the wall-normal velocity; needs a symmetric velocity axis) */
+#define MM2D_FACE_SPECULAR 3
 
 /* collision models (gas_state.py:166-199) */
 #define MM2D_TAU_HARD_SPHERE_1D 0

@@ -20,7 +20,13 @@
  * Layouts (C-contiguous fp64, identical to the reference):
  *   2D: Q[i][j][6], G[i][j][k][l] (l fastest), H[4][i][j]
  *   1D: Q[i][3],    G[i][k]
- * Face kinds: 0 periodic, 1 extrapolate, 2 diffuse wall.
+ * Face kinds: 0 periodic, 1 extrapolate, 2 diffuse wall, 3 specular wall.
+ * Specular walls are an EXTENSION (BASELINE config 4 wording; the reference
+ * has only diffuse walls): every ghost is the mirror image of the edge cell
+ * in the wall-normal velocity, v_n -> -v_n (micro ghosts: node index
+ * reversed along the normal axis; macro ghosts: normal momentum and E12
+ * negated; heat ghosts: components odd in v_n negated).  Parity of this
+ * rule is unpinned (no reference implementation exists).
  */
 #include <math.h>
 #include <stdlib.h>
@@ -34,7 +40,7 @@
 #define PI_D 3.141592653589793238462643383279502884
 #define SQRT2_D 1.4142135623730950488016887242096980786
 
-enum { FACE_PERIODIC = 0, FACE_EXTRAPOLATE = 1, FACE_WALL = 2 };
+enum { FACE_PERIODIC = 0, FACE_EXTRAPOLATE = 1, FACE_WALL = 2, FACE_SPECULAR = 3 };
 enum { TAU_HARD_SPHERE_1D = 0, TAU_PRESSURE_1D = 1, TAU_ESBGK_2D = 2,
        TAU_BGK_2D = 3, TAU_CONSTANT = 4 };
 
@@ -415,7 +421,19 @@ void mmo_project_field_1d(int nx, int nv, const double *F, const double *M,
 /* 2D boundary machinery: boundary.py:181-378                                */
 /* ------------------------------------------------------------------------ */
 
-/* extend_micro_2d (boundary.py:181-210): wrap / copy edge / zero (wall) */
+/* specular ghost of one cell: the edge cell mirrored in v_n (axis 0: k
+ * reversed, axis 1: l reversed) */
+static void mirror_cell(const mmo_cfg2d *cf, const double *edge, int axis, double *dst)
+{
+    int nv1 = cf->nv1, nv2 = cf->nv2;
+    for (int k = 0; k < nv1; ++k)
+        for (int l = 0; l < nv2; ++l)
+            dst[k * nv2 + l] = axis == 0 ? edge[(nv1 - 1 - k) * nv2 + l]
+                                         : edge[k * nv2 + (nv2 - 1 - l)];
+}
+
+/* extend_micro_2d (boundary.py:181-210): wrap / copy edge / zero (wall) /
+ * mirror (specular extension) */
 static void extend_micro(const mmo_cfg2d *cf, const double *G, int axis, double *G_ext)
 {
     int nx = cf->nx, ny = cf->ny;
@@ -430,9 +448,15 @@ static void extend_micro(const mmo_cfg2d *cf, const double *G, int axis, double 
             return;
         }
         if (lo == FACE_EXTRAPOLATE) memcpy(G_ext, G, row * sizeof(double));
+        else if (lo == FACE_SPECULAR)
+            for (int j = 0; j < ny; ++j) mirror_cell(cf, G + (size_t)j * V, 0, G_ext + (size_t)j * V);
         else memset(G_ext, 0, row * sizeof(double));
         if (hi == FACE_EXTRAPOLATE)
             memcpy(G_ext + (size_t)(nx + 1) * row, G + (size_t)(nx - 1) * row, row * sizeof(double));
+        else if (hi == FACE_SPECULAR)
+            for (int j = 0; j < ny; ++j)
+                mirror_cell(cf, G + (size_t)((nx - 1) * ny + j) * V, 0,
+                            G_ext + (size_t)((nx + 1) * ny + j) * V);
         else memset(G_ext + (size_t)(nx + 1) * row, 0, row * sizeof(double));
     } else {
         int eny = ny + 2;
@@ -446,24 +470,34 @@ static void extend_micro(const mmo_cfg2d *cf, const double *G, int axis, double 
                 memcpy(dst + (size_t)(ny + 1) * V, src, V * sizeof(double));
             } else {
                 if (lo == FACE_EXTRAPOLATE) memcpy(dst, src, V * sizeof(double));
+                else if (lo == FACE_SPECULAR) mirror_cell(cf, src, 1, dst);
                 else memset(dst, 0, V * sizeof(double));
                 if (hi == FACE_EXTRAPOLATE)
                     memcpy(dst + (size_t)(ny + 1) * V, src + (size_t)(ny - 1) * V, V * sizeof(double));
+                else if (hi == FACE_SPECULAR)
+                    mirror_cell(cf, src + (size_t)(ny - 1) * V, 1, dst + (size_t)(ny + 1) * V);
                 else memset(dst + (size_t)(ny + 1) * V, 0, V * sizeof(double));
             }
         }
     }
 }
 
-/* extend_macro_scalar_2d (boundary.py:213-221): wrap for periodic else copy */
-static double ext_scalar(const mmo_cfg2d *cf, const double *f, int i, int j)
+/* extend_macro_scalar_2d (boundary.py:213-221): wrap for periodic else copy;
+ * at a specular face the ghost of a field odd in that axis' velocity (u1 in
+ * x, u2 in y) is the negated edge value (odd_x / odd_y) */
+static double ext_scalar(const mmo_cfg2d *cf, const double *f, int i, int j, int odd_x, int odd_y)
 {
     int nx = cf->nx, ny = cf->ny;
+    double sg = 1.0;
+    if ((i < 0 && cf->face[0] == FACE_SPECULAR) || (i >= nx && cf->face[1] == FACE_SPECULAR))
+        if (odd_x) sg = -sg;
+    if ((j < 0 && cf->face[2] == FACE_SPECULAR) || (j >= ny && cf->face[3] == FACE_SPECULAR))
+        if (odd_y) sg = -sg;
     if (i < 0) i = cf->face[0] == FACE_PERIODIC ? nx - 1 : 0;
     if (i >= nx) i = cf->face[0] == FACE_PERIODIC ? 0 : nx - 1;
     if (j < 0) j = cf->face[2] == FACE_PERIODIC ? ny - 1 : 0;
     if (j >= ny) j = cf->face[2] == FACE_PERIODIC ? 0 : ny - 1;
-    return f[i * ny + j];
+    return sg < 0.0 ? -f[i * ny + j] : f[i * ny + j];
 }
 
 static const int SIGN_2D[4] = { -1, +1, -1, +1 };   /* boundary.py:263 */
@@ -538,6 +572,10 @@ static void ghat_override(const mmo_cfg2d *cf, double *Ghat, const double *M,
                         for (int k = 0; k < nv1; ++k)
                             for (int l = 0; l < nv2; ++l)
                                 Mn[f][k * nv2 + l] = wall_maxwellian(g[0], g[1], g[2], cf->wall_T[face], v1[k], v2[l]);
+                        continue;
+                    }
+                    if (outside && cf->face[face] == FACE_SPECULAR) {
+                        mirror_cell(cf, M + (size_t)c * V, face < 2 ? 0 : 1, Mn[f]);
                         continue;
                     }
                     if (outside) {
@@ -652,6 +690,13 @@ static void pstate(const prim2 *p, double s[6])
 static void ghost_pstate(const mmo_cfg2d *cf, int face, const double edge[6], double s[6])
 {
     if (cf->face[face] == FACE_EXTRAPOLATE) { memcpy(s, edge, 6 * sizeof(double)); return; }
+    if (cf->face[face] == FACE_SPECULAR) {
+        /* mirror image: normal velocity and P12 change sign */
+        memcpy(s, edge, 6 * sizeof(double));
+        s[face < 2 ? 1 : 2] = -edge[face < 2 ? 1 : 2];
+        s[4] = -edge[4];
+        return;
+    }
     double rho = edge[0];
     double t11 = edge[3] / rho, t22 = edge[5] / rho;
     double g[6];
@@ -660,15 +705,22 @@ static void ghost_pstate(const mmo_cfg2d *cf, int face, const double edge[6], do
     s[3] = g[0] * g[3]; s[4] = g[0] * g[4]; s[5] = g[0] * g[5];
 }
 
-/* interface_heat_2d (boundary.py:224-241) at interface index m in [0, n] */
+/* interface_heat_2d (boundary.py:224-241) at interface index m in [0, n].
+ * Specular faces: mean of the edge value and its mirror image, which is
+ * -edge for the components odd in v_n (odd != 0). */
 static double iface_heat(const mmo_cfg2d *cf, int axis, const double *h, int n,
-                         int stride, int m)
+                         int stride, int m, int odd)
 {
     int lo = cf->face[axis == 0 ? 0 : 2], hi = cf->face[axis == 0 ? 1 : 3];
     if (m > 0 && m < n) return 0.5 * (h[m * stride] + h[(m - 1) * stride]);
     if (lo == FACE_PERIODIC) return 0.5 * (h[0] + h[(n - 1) * stride]);
-    if (m == 0) return lo == FACE_EXTRAPOLATE ? h[0] : 0.5 * h[0];
-    return hi == FACE_EXTRAPOLATE ? h[(n - 1) * stride] : 0.5 * h[(n - 1) * stride];
+    if (m == 0) {
+        if (lo == FACE_SPECULAR) return 0.5 * (h[0] + (odd ? -h[0] : h[0]));
+        return lo == FACE_EXTRAPOLATE ? h[0] : 0.5 * h[0];
+    }
+    double e = h[(n - 1) * stride];
+    if (hi == FACE_SPECULAR) return 0.5 * ((odd ? -e : e) + e);
+    return hi == FACE_EXTRAPOLATE ? e : 0.5 * e;
 }
 
 /* _sweep (macro2d.py:206-221) along `axis`; hc = the three H components */
@@ -716,8 +768,10 @@ static int sweep(const mmo_cfg2d *cf, const double *Q, const double *const hc[3]
             const double *hl = axis == 0 ? h + line : h + (size_t)line * ny;
             for (int p = 0; p < len; ++p) {
                 int c = CELL(p);
-                double hp = iface_heat(cf, axis, hl, len, stride, p + 1);
-                double hm = iface_heat(cf, axis, hl, len, stride, p);
+                /* H111, H122 odd in v1; H112, H222 odd in v2: in both sweeps
+                 * the components t = 0 and 2 are the odd ones */
+                double hp = iface_heat(cf, axis, hl, len, stride, p + 1, t != 1);
+                double hm = iface_heat(cf, axis, hl, len, stride, p, t != 1);
                 Qn[6 * c + 3 + t] -= r * (hp - hm);
             }
         }
@@ -777,14 +831,14 @@ int mmo_step_2d(const mmo_cfg2d *cf, const double *Q, const double *G, double dt
     for (int i = 0; i < nx; ++i)
         for (int j = 0; j < ny; ++j) {
             int c = i * ny + j;
-            double du1x = (ext_scalar(cf, u1, i + 1, j) - ext_scalar(cf, u1, i - 1, j)) / (2.0 * cf->dx);
-            double du2x = (ext_scalar(cf, u2, i + 1, j) - ext_scalar(cf, u2, i - 1, j)) / (2.0 * cf->dx);
-            double du1y = (ext_scalar(cf, u1, i, j + 1) - ext_scalar(cf, u1, i, j - 1)) / (2.0 * cf->dy);
-            double du2y = (ext_scalar(cf, u2, i, j + 1) - ext_scalar(cf, u2, i, j - 1)) / (2.0 * cf->dy);
+            double du1x = (ext_scalar(cf, u1, i + 1, j, 1, 0) - ext_scalar(cf, u1, i - 1, j, 1, 0)) / (2.0 * cf->dx);
+            double du2x = (ext_scalar(cf, u2, i + 1, j, 0, 1) - ext_scalar(cf, u2, i - 1, j, 0, 1)) / (2.0 * cf->dx);
+            double du1y = (ext_scalar(cf, u1, i, j + 1, 1, 0) - ext_scalar(cf, u1, i, j - 1, 1, 0)) / (2.0 * cf->dy);
+            double du2y = (ext_scalar(cf, u2, i, j + 1, 0, 1) - ext_scalar(cf, u2, i, j - 1, 0, 1)) / (2.0 * cf->dy);
             s11[c] = du1x - du2y;
             s12[c] = du1y + du2x;
-            gT1[c] = (ext_scalar(cf, T, i + 1, j) - ext_scalar(cf, T, i - 1, j)) / (2.0 * cf->dx);
-            gT2[c] = (ext_scalar(cf, T, i, j + 1) - ext_scalar(cf, T, i, j - 1)) / (2.0 * cf->dy);
+            gT1[c] = (ext_scalar(cf, T, i + 1, j, 0, 0) - ext_scalar(cf, T, i - 1, j, 0, 0)) / (2.0 * cf->dx);
+            gT2[c] = (ext_scalar(cf, T, i, j + 1, 0, 0) - ext_scalar(cf, T, i, j - 1, 0, 0)) / (2.0 * cf->dy);
         }
     mmo_ghat_2d(nx, ny, nv1, nv2, M, u1, u2, T, s11, s12, gT1, gT2, tau, v1, v2, Ghat);
     if (cf->nu != 0.0) {

@@ -22,7 +22,7 @@ import numpy as np
 _HERE = Path(__file__).resolve().parent
 _LIB_PATH = _HERE / "_build" / "libmm_oracle.so"
 
-FACE_PERIODIC, FACE_EXTRAPOLATE, FACE_WALL = 0, 1, 2
+FACE_PERIODIC, FACE_EXTRAPOLATE, FACE_WALL, FACE_SPECULAR = 0, 1, 2, 3
 TAU_KINDS = {"hard_sphere_1d": 0, "pressure_1d": 1, "esbgk_2d": 2,
              "bgk_2d": 3, "constant": 4}
 ERR_MESSAGES = {1: "non-positive density",
@@ -109,7 +109,8 @@ def _centers(axis):
 
 def _face_code(face):
     if isinstance(face, str):
-        return {"periodic": FACE_PERIODIC, "extrapolate": FACE_EXTRAPOLATE}[face]
+        return {"periodic": FACE_PERIODIC, "extrapolate": FACE_EXTRAPOLATE,
+                "specular": FACE_SPECULAR}[face]
     return FACE_WALL
 
 

@@ -5,7 +5,7 @@ and friends): the same problem objects and functional API, with the step
 fused into hand-written sm_100a CUDA kernels (csrc/, C ABI in include/mm2d.h).
 """
 
-from .boundary import (EXTRAPOLATE, EXTRAPOLATE_1D, PERIODIC, PERIODIC_1D,
+from .boundary import (EXTRAPOLATE, EXTRAPOLATE_1D, PERIODIC, PERIODIC_1D, SPECULAR,
                        BoundarySpec1D, BoundarySpec2D, WallSpec)
 from .errors import ConfigurationError, InvalidStateError, NativeLibraryError
 from .gas_state import (CollisionModel, TempTensor2D, conserved_1d, conserved_2d,
@@ -34,7 +34,7 @@ def __getattr__(name):
 
 
 __all__ = ["Axis", "PhaseMesh", "TimePlan", "cell_centers", "plan_time", "PERIODIC",
-           "EXTRAPOLATE", "PERIODIC_1D", "EXTRAPOLATE_1D", "WallSpec", "BoundarySpec1D",
+           "EXTRAPOLATE", "SPECULAR", "PERIODIC_1D", "EXTRAPOLATE_1D", "WallSpec", "BoundarySpec1D",
            "BoundarySpec2D", "CollisionModel", "TempTensor2D", "conserved_1d",
            "conserved_2d", "primitives_1d", "primitives_2d", "ConfigurationError",
            "InvalidStateError", "NativeLibraryError", "State2D", "step_2d", "run_2d",

@@ -1,8 +1,15 @@
 """Boundary specifications (drop-in for pkg/src/micromacro/boundary.py:21-81).
 
-Face kinds: ``PERIODIC`` (paired), ``EXTRAPOLATE`` (zero-gradient copy) and
+Face kinds: ``PERIODIC`` (paired), ``EXTRAPOLATE`` (zero-gradient copy),
 ``WallSpec`` (diffusely reflecting wall at fixed temperature, optional
-tangential velocity).  The ghost-cell rules themselves run on the device
+tangential velocity) and ``SPECULAR`` (specularly reflecting wall, 2D only).
+
+``SPECULAR`` is an extension beyond the reference, which has diffuse walls
+only (BASELINE config 4 asks for reflecting walls).  Every ghost is the
+mirror image of the edge cell in the wall-normal velocity: micro ghosts take
+the edge distribution at v_n -> -v_n, macro ghosts negate the normal
+momentum and E12, heat ghosts negate the components odd in v_n.  It needs a
+velocity axis symmetric about zero along the wall normal.  The ghost-cell rules themselves run on the device
 (csrc/mm2d_prep.cuh, mm2d_micro.cuh, mm2d_macro.cuh).
 """
 
@@ -14,6 +21,7 @@ from .errors import ConfigurationError
 
 PERIODIC = "periodic"
 EXTRAPOLATE = "extrapolate"
+SPECULAR = "specular"
 
 
 @dataclass(frozen=True)
@@ -36,7 +44,7 @@ def is_wall(face) -> bool:
 
 
 def _validate_face(face):
-    if face in (PERIODIC, EXTRAPOLATE) or is_wall(face):
+    if face in (PERIODIC, EXTRAPOLATE, SPECULAR) or is_wall(face):
         return
     raise ConfigurationError(f"unknown boundary face {face!r}")
 
@@ -54,6 +62,8 @@ class BoundarySpec1D:
     def __post_init__(self):
         for f in (self.left, self.right):
             _validate_face(f)
+            if f == SPECULAR:
+                raise ConfigurationError("specular walls are supported in 2D only")
         _paired(self.left, self.right, "boundaries")
 
 
@@ -86,15 +96,17 @@ EXTRAPOLATE_1D = BoundarySpec1D(EXTRAPOLATE, EXTRAPOLATE)
 
 
 def face_code(face) -> int:
-    """0 periodic, 1 extrapolate, 2 wall (include/mm2d.h MM2D_FACE_*)."""
+    """0 periodic, 1 extrapolate, 2 wall, 3 specular (include/mm2d.h MM2D_FACE_*)."""
     if face == PERIODIC:
         return 0
     if face == EXTRAPOLATE:
         return 1
     if is_wall(face):
         return 2
+    if face == SPECULAR:
+        return 3
     raise ConfigurationError(f"unknown boundary face {face!r}")
 
 
-__all__ = ["PERIODIC", "EXTRAPOLATE", "WallSpec", "BoundarySpec1D", "BoundarySpec2D",
+__all__ = ["PERIODIC", "EXTRAPOLATE", "SPECULAR", "WallSpec", "BoundarySpec1D", "BoundarySpec2D",
            "PERIODIC_1D", "EXTRAPOLATE_1D", "face_code", "is_wall"]

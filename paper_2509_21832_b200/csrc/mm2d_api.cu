@@ -106,11 +106,13 @@ static const void* pick_micro(int NE, int BX, bool fast) {
 }
 
 static int ghost_mode(const mm2d_config& c, int face, bool at_edge, int nranks_axis, int field) {
-    // field 0: micro G (walls zero), 1: macro Q (walls copy), 2: heat (walls zero)
+    // field 0: micro G (walls zero), 1: macro Q (walls copy), 2: heat (walls zero);
+    // specular walls mirror every field
     if (!at_edge) return GM_HALO;
     const int kind = c.face[face];
     if (kind == MM2D_FACE_PERIODIC) return nranks_axis > 1 ? GM_HALO : GM_WRAP;
     if (kind == MM2D_FACE_EXTRAPOLATE) return GM_COPY;
+    if (kind == MM2D_FACE_SPECULAR) return GM_MIRROR;
     return field == 1 ? GM_COPY : GM_ZERO;
 }
 
@@ -139,7 +141,7 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         return r;
     }
     for (int f = 0; f < 4; ++f)
-        if (c.face[f] < 0 || c.face[f] > 2) {
+        if (c.face[f] < 0 || c.face[f] > 3) {
             int r = fail_cfg(ctx, "unknown face kind");
             delete ctx;
             return r;
@@ -149,6 +151,21 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         int r = fail_cfg(ctx, "periodic boundaries must come in pairs");
         delete ctx;
         return r;
+    }
+    {
+        // specular faces mirror the node index along the wall normal, which is
+        // the reflection v_n -> -v_n only on an axis symmetric about zero
+        const double lo[2] = {c.v1_min, c.v2_min}, hi[2] = {c.v1_max, c.v2_max};
+        for (int f = 0; f < 4; ++f) {
+            if (c.face[f] != MM2D_FACE_SPECULAR) continue;
+            const int ax = f < 2 ? 0 : 1;
+            if (!(std::fabs(lo[ax] + hi[ax]) <= 1e-14 * (hi[ax] - lo[ax]))) {
+                int r = fail_cfg(ctx, "specular walls need a velocity axis symmetric about zero "
+                                      "along the wall normal");
+                delete ctx;
+                return r;
+            }
+        }
     }
     if (!(c.nu >= -1.0 && c.nu < 1.0)) {
         int r = fail_cfg(ctx, "nu must lie in [-1, 1)");

@@ -27,7 +27,10 @@ enum FaceKind { FACE_PERIODIC = 0, FACE_EXTRAPOLATE = 1, FACE_WALL = 2 };
 //   COPY: zero-gradient copy of the edge layer (extrapolate; walls for macro)
 //   ZERO: zero ghost (micro / heat fields at diffuse walls)
 //   HALO: received from a neighbour rank (interior or periodic-across-ranks)
-enum GhostMode { GM_WRAP = 0, GM_COPY = 1, GM_ZERO = 2, GM_HALO = 3 };
+// GM_MIRROR: specular wall (extension) -- the ghost is the edge cell mirrored
+// in the wall-normal velocity (G: node index reversed along the normal axis;
+// Q: normal momentum and E12 negated; H: components odd in v_n negated)
+enum GhostMode { GM_WRAP = 0, GM_COPY = 1, GM_ZERO = 2, GM_HALO = 3, GM_MIRROR = 4 };
 
 // stage/check codes of the sticky error word; the key orders failures the
 // way the reference raises them within one step (loop.py:98, micro2d.py:92,

@@ -193,6 +193,7 @@ __global__ void k_macro_y(MacroArgs a) {
         if (j == 0 && g.qylo != GM_HALO && g.qylo != GM_WRAP) {
             if (g.wall[2]) wall_pstate(g, 2, sc, sd);
             else for (int m = 0; m < 6; ++m) sd[m] = sc[m];
+            if (g.qylo == GM_MIRROR) { sd[2] = -sd[2]; sd[4] = -sd[4]; }   // specular image
         } else {
             const int jj = (j == 0 && g.qylo == GM_WRAP) ? g.by - 1 : j - 1;
             pstate(a.Qx + 6 * ring_index(g, i, jj), sd);
@@ -200,6 +201,7 @@ __global__ void k_macro_y(MacroArgs a) {
         if (j == g.by - 1 && g.qyhi != GM_HALO && g.qyhi != GM_WRAP) {
             if (g.wall[3]) wall_pstate(g, 3, sc, su);
             else for (int m = 0; m < 6; ++m) su[m] = sc[m];
+            if (g.qyhi == GM_MIRROR) { su[2] = -su[2]; su[4] = -su[4]; }   // specular image
         } else {
             const int jj = (j == g.by - 1 && g.qyhi == GM_WRAP) ? 0 : j + 1;
             pstate(a.Qx + 6 * ring_index(g, i, jj), su);

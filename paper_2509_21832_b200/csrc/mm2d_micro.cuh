@@ -52,10 +52,14 @@ struct MicroArgs {
     double dt, eps, inveps, idx, idy, dv, hfac;  // hfac = eps * dv
 };
 
-// Pointer to G^n of ring cell (i, r) or nullptr for a zero ghost.
-__device__ __forceinline__ const double* gn_cell(const MicroArgs& a, int i, int r) {
+// Pointer to G^n of ring cell (i, r) or nullptr for a zero ghost.  *mir is
+// set when the cell is the specular image (k reversed) of the returned one;
+// rows of a specular y face are never read here (row_kind 3).
+__device__ __forceinline__ const double* gn_cell(const MicroArgs& a, int i, int r,
+                                                 bool* mir = nullptr) {
     const Geometry& g = a.g;
     const size_t V = (size_t)g.V;
+    if (mir) *mir = false;
     bool yhalo = false;
     int rr = r;
     if (r < 0 || r >= g.by) {
@@ -75,18 +79,20 @@ __device__ __forceinline__ const double* gn_cell(const MicroArgs& a, int i, int 
         }
         if (m == GM_WRAP) ii = (i + g.bx) % g.bx;
         else ii = i < 0 ? 0 : g.bx - 1;
+        if (m == GM_MIRROR && mir) *mir = true;
     }
     if (yhalo) return (r < 0 ? a.hylo : a.hyhi) + (size_t)(ii + 1) * V;
     return a.G + ((size_t)ii * g.by + rr) * V;
 }
 
 // How a ring row r is obtained for the y-stage ghosts of G*:
-//   0 compute the x-stage on it, 1 copy of the adjacent owned row, 2 zero.
+//   0 compute the x-stage on it, 1 copy of the adjacent owned row, 2 zero,
+//   3 specular image of the adjacent owned row (l reversed).
 __device__ __forceinline__ int row_kind(const Geometry& g, int r) {
     if (r >= 0 && r < g.by) return 0;
     const int m = r < 0 ? g.ylo : g.yhi;
     if (m == GM_WRAP || m == GM_HALO) return 0;
-    return m == GM_COPY ? 1 : 2;
+    return m == GM_COPY ? 1 : m == GM_MIRROR ? 3 : 2;
 }
 
 // Per-cell tables in shared memory for one row slot:
@@ -272,9 +278,20 @@ __global__ void __launch_bounds__(256) k_micro(MicroArgs a) {
     auto prefetch = [&](int r) {
 #pragma unroll
         for (int b = 0; b < BX; ++b) nm.load(b < nb ? gn_cell(a, ic0 + b, r) : nullptr, pf[b]);
-        const double* hl = gn_cell(a, ic0 - 1, r);
-        const double* hr = gn_cell(a, ic0 + nb, r);
-        if (FAST) {
+        bool ml, mr;
+        const double* hl = gn_cell(a, ic0 - 1, r, &ml);
+        const double* hr = gn_cell(a, ic0 + nb, r, &mr);
+        if (ml || mr) {
+            // specular x face: the halo node (k, l) is the edge cell's (nv1-1-k, l)
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                const bool left = v1s[nm.k[e]] >= 0.0;
+                const double* hp = left ? hl : hr;
+                const bool m = left ? ml : mr;
+                const int node = m ? (nv1 - 1 - nm.k[e]) * nv2 + nm.l[e] : nm.node[e];
+                ph[e] = (hp != nullptr && nm.ok[e]) ? __ldg(hp + node) : 0.0;
+            }
+        } else if (FAST) {
 #pragma unroll
             for (int e = 0; e < NE; e += 2) {
                 const double* hp = v1s[nm.k[e]] >= 0.0 ? hl : hr;
@@ -343,12 +360,18 @@ __global__ void __launch_bounds__(256) k_micro(MicroArgs a) {
         }
     };
 
-    auto fill_row = [&](int r, int kind, int src) {   // copy (kind 1) or zero (kind 2)
+    auto fill_row = [&](int r, int kind, int src) {   // copy (1), zero (2) or mirror (3)
+        if (kind == 3) __syncthreads();   // the source row was stored by other threads
 #pragma unroll
         for (int b = 0; b < BX; ++b) {
             double o[NE];
             if (kind == 1) nm.sload(gs_ptr(src, b), o);
-            else {
+            else if (kind == 3) {
+                const double* sr = gs_ptr(src, b);
+#pragma unroll
+                for (int e = 0; e < NE; ++e)
+                    o[e] = nm.ok[e] ? sr[nm.k[e] * nv2 + (nv2 - 1 - nm.l[e])] : 0.0;
+            } else {
 #pragma unroll
                 for (int e = 0; e < NE; ++e) o[e] = 0.0;
             }

@@ -471,7 +471,9 @@ inline size_t smem_bytes_v3() {
 // are accumulated as A_a = sum W1^a o per node column, then weighted by the
 // thread's W2 powers.  The row loop runs a predicate-free body for the rows
 // away from the piece ends.
-template <int NP_>
+// MIR: the instantiation for problems with a specular face (the others are
+// compiled without any mirror code, so the benchmark path's code is untouched)
+template <int NP_, bool MIR>
 __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a) {
     static_assert(NP_ == 4, "the TMEM ring is laid out for 4 node pairs per thread");
     constexpr int NT_ = 512 / NP_;       // threads per CTA
@@ -538,13 +540,22 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     if (i > 0) lft_b = own_b - (size_t)g.by * V_;
     else if (g.xlo == GM_HALO) lft_b = a.hxlo;
     else if (g.xlo == GM_WRAP) lft_b = a.G + (size_t)(g.bx - 1) * g.by * V_;
-    else if (g.xlo == GM_COPY) lft_b = own_b;
+    else if (g.xlo == GM_COPY || (MIR && g.xlo == GM_MIRROR)) lft_b = own_b;
     else { lft_b = a.zero; lft_s = 0; }
     if (i < g.bx - 1) rgt_b = own_b + (size_t)g.by * V_;
     else if (g.xhi == GM_HALO) rgt_b = a.hxhi;
     else if (g.xhi == GM_WRAP) rgt_b = a.G;
-    else if (g.xhi == GM_COPY) rgt_b = own_b;
+    else if (g.xhi == GM_COPY || (MIR && g.xhi == GM_MIRROR)) rgt_b = own_b;
     else { rgt_b = a.zero; rgt_s = 0; }
+    // specular x faces: the upwind neighbour of node (k, l) is the edge cell's
+    // own node (31 - k, l), already staged with the own row, so the x-stage
+    // reads it from there (the halo copy of these CTAs is unused).  These
+    // columns run every row through the general body, so the steady body
+    // carries no mirror test.
+    // (recomputed at the use sites from blockIdx / the constant bank so they
+    // hold no registers across the steady loop)
+    auto mir_l = [&]() { return MIR && blockIdx.x == 0 && g.xlo == GM_MIRROR; };
+    auto mir_r = [&]() { return MIR && (int)blockIdx.x == g.bx - 1 && g.xhi == GM_MIRROR; };
 
     const bool on_x = (g.wall[0] && i == 0) || (g.wall[1] && i == g.bx - 1);
     const double* wx = on_x ? a.wall_ghat + ((size_t)(i == 0 ? 0 : 1) * g.by) * V_ : nullptr;
@@ -639,6 +650,25 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     // x-stage: c depends on k only, so the K-table carries (c w1, c h1).
     // y-stage: c depends on l only (cy0, cy1), applied once per thread.
 
+    // G* row mirrored in v2 (l -> 31 - l) for specular y faces: the image of
+    // this thread's pair (lb, lb+1) is pair 30 - lb of the thread with the
+    // same k base in the partner warp (tid ^ 0x27), swapped.  Exchanged
+    // through the (idle) reduction partials; CTA-uniform call sites only.
+    auto mirror_l = [&](double (&v)[2 * NP_]) {
+        double* xch = sred;
+#pragma unroll
+        for (int q = 0; q < 2 * NP_; q += 2) sts2(xch + 2 * NP_ * tid + q, v[q], v[q + 1]);
+        __syncthreads();
+        const int pt = tid ^ 0x27;
+#pragma unroll
+        for (int q = 0; q < 2 * NP_; q += 2) {
+            const double2 x = lds2(xch + 2 * NP_ * pt + q);
+            v[q] = x.y;
+            v[q + 1] = x.x;
+        }
+        __syncthreads();
+    };
+
     auto body = [&](int j, auto steady) {
         constexpr bool ST = decltype(steady)::value;
         const int rx = j + 2;       // x-stage row
@@ -671,9 +701,12 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             }
             tm_st8(R2, gst);
         } else if ((rc == j1s && k_hi != 0) || (rc == j0s - 1 && k_lo == 2)) {
-            // ghost rows: zero (wall) or copy of the adjacent owned row
+            // ghost rows: zero (wall), copy or specular image of the adjacent owned row
             if (rc == j1s && k_hi == 1) tm_ld8(R1, gst);
-            else {
+            else if (MIR && rc == j1s && k_hi == 3) {
+                tm_ld8(R1, gst);
+                mirror_l(gst);
+            } else {
 #pragma unroll
                 for (int q = 0; q < 2 * NP_; ++q) gst[q] = 0.0;
             }
@@ -682,9 +715,14 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
 #pragma unroll
             for (int q = 0; q < 2 * NP_; ++q) gst[q] = 0.0;
         }
-        if (!ST && rc == j0s && k_lo == 1) {   // bottom ghost by copy, once G*(j0s) is complete
+        if (!ST && rc == j0s && (k_lo == 1 || (MIR && k_lo == 3))) {
+            // bottom ghost by copy / specular image, once G*(j0s) is complete
+            double gb[2 * NP_];
+#pragma unroll
+            for (int q = 0; q < 2 * NP_; ++q) gb[q] = gst[q];
+            if (MIR && k_lo == 3) mirror_l(gb);
             tm_wait_st();
-            tm_st8(R1, gst);
+            tm_st8(R1, gb);
         }
         double s[12];
 #pragma unroll
@@ -731,7 +769,9 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             double Y0, Y1, S1, S3;
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
-                const double2 c = lds2(stg + off_(p)), h = lds2(stg + V + off_(p));
+                const bool mir = MIR && !ST && (p < NP_ / 2 ? mir_r() : mir_l());
+                const double2 c = lds2(stg + off_(p));
+                const double2 h = lds2(stg + (mir ? NV * (NV - 1 - kb - KS * p) + lb : V + off_(p)));
                 const double d0 = c.x - h.x, d1 = c.y - h.y;
                 xs[2 * p] = fma(-cx[p], d0, c.x);
                 xs[2 * p + 1] = fma(-cx[p], d1, c.y);
@@ -886,7 +926,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     };
 
     // steady rows: every stage active, no ghost rows, no wall rows
-    const int js_lo = j0s + 1, js_hi = min(rhi - 5, j1s - 1);
+    const int js_lo = j0s + 1, js_hi = (MIR && (mir_l() || mir_r())) ? js_lo - 1 : min(rhi - 5, j1s - 1);
     int j = j0s - 4;
     for (; j < js_lo && j <= j1s; ++j) body(j, std::false_type());
     for (; j <= js_hi; ++j) body(j, std::true_type());

@@ -11,18 +11,22 @@ namespace mm2d {
 //   returns 0: interior cell (si, sj) of the source block
 //           1: ring cell (si, sj) that holds received halo data
 //           2: zero
+// flip: bit 0 the source is mirrored in v1 (specular x face), bit 1 in v2.
 enum { RS_INTERIOR = 0, RS_RING = 1, RS_ZERO = 2 };
 
 __device__ __forceinline__ int resolve_ring(int bx, int by, int mxlo, int mxhi, int mylo,
-                                            int myhi, int i, int j, int& si, int& sj) {
+                                            int myhi, int i, int j, int& si, int& sj,
+                                            int& flip) {
     bool yhalo = false;
     int jj = j;
+    flip = 0;
     if (j < 0 || j >= by) {
         const int m = j < 0 ? mylo : myhi;
         if (m == GM_ZERO) return RS_ZERO;
         if (m == GM_HALO) yhalo = true;
         else if (m == GM_WRAP) jj = (j + by) % by;
         else jj = j < 0 ? 0 : by - 1;
+        if (m == GM_MIRROR) flip |= 2;
     }
     int ii = i;
     if (i < 0 || i >= bx) {
@@ -31,9 +35,24 @@ __device__ __forceinline__ int resolve_ring(int bx, int by, int mxlo, int mxhi, 
         if (m == GM_HALO) { si = i; sj = jj; return RS_RING; }
         if (m == GM_WRAP) ii = (i + bx) % bx;
         else ii = i < 0 ? 0 : bx - 1;
+        if (m == GM_MIRROR) flip |= 1;
     }
     si = ii; sj = jj;
     return yhalo ? RS_RING : RS_INTERIOR;
+}
+
+// sign of conserved component c of a mirrored ghost: rho u1 flips with v1,
+// rho u2 with v2, E12 with either
+__device__ __forceinline__ double q_mirror_sign(int c, int flip) {
+    const int odd = (c == 1 ? (flip & 1) : 0) ^ (c == 2 ? (flip >> 1) : 0) ^
+                    (c == 4 ? ((flip & 1) ^ (flip >> 1)) : 0);
+    return odd ? -1.0 : 1.0;
+}
+// heat component c (H111, H112, H122, H222): odd in v1 for c = 0, 2, odd in
+// v2 for c = 1, 3
+__device__ __forceinline__ double h_mirror_sign(int c, int flip) {
+    const int odd = ((c == 0 || c == 2) ? (flip & 1) : (flip >> 1));
+    return odd ? -1.0 : 1.0;
 }
 
 // Fill the ghost ring of Qr from the owned block Q (bx, by, 6).  Cells that
@@ -44,18 +63,18 @@ __global__ void k_fill_qring(Geometry g, const double* __restrict__ Q, double* _
     const int n = (g.bx + 2) * (g.by + 2);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
-        int si, sj;
-        const int rs = resolve_ring(g.bx, g.by, g.qxlo, g.qxhi, g.qylo, g.qyhi, i, j, si, sj);
+        int si, sj, flip;
+        const int rs = resolve_ring(g.bx, g.by, g.qxlo, g.qxhi, g.qylo, g.qyhi, i, j, si, sj, flip);
         double* dst = Qr + 6 * t;
         if (rs == RS_INTERIOR) {
             const double* src = Q + 6 * ((size_t)si * g.by + sj);
 #pragma unroll
-            for (int c = 0; c < 6; ++c) dst[c] = src[c];
+            for (int c = 0; c < 6; ++c) dst[c] = flip ? q_mirror_sign(c, flip) * src[c] : src[c];
         } else if (rs == RS_RING) {
             if (si == i && sj == j) continue;   // received directly
             const double* src = Qr + 6 * ring_index(g, si, sj);
 #pragma unroll
-            for (int c = 0; c < 6; ++c) dst[c] = src[c];
+            for (int c = 0; c < 6; ++c) dst[c] = flip ? q_mirror_sign(c, flip) * src[c] : src[c];
         } else {
 #pragma unroll
             for (int c = 0; c < 6; ++c) dst[c] = 0.0;
@@ -72,8 +91,8 @@ __global__ void k_fill_hring(Geometry g, double* __restrict__ Hr) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
         if (i >= 0 && i < g.bx && j >= 0 && j < g.by) continue;
-        int si, sj;
-        const int rs = resolve_ring(g.bx, g.by, g.hxlo, g.hxhi, g.hylo, g.hyhi, i, j, si, sj);
+        int si, sj, flip;
+        const int rs = resolve_ring(g.bx, g.by, g.hxlo, g.hxhi, g.hylo, g.hyhi, i, j, si, sj, flip);
         double* dst = Hr + 4 * t;
         if (rs == RS_ZERO) {
 #pragma unroll
@@ -82,7 +101,7 @@ __global__ void k_fill_hring(Geometry g, double* __restrict__ Hr) {
             if (rs == RS_RING && si == i && sj == j) continue;
             const double* src = Hr + 4 * ring_index(g, si, sj);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) dst[c] = src[c];
+            for (int c = 0; c < 4; ++c) dst[c] = flip ? h_mirror_sign(c, flip) * src[c] : src[c];
         }
     }
 }
