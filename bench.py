@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the micro-macro ES-BGK 2D2V timestep on B200.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c5|weak]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c3|c4|c4s|c5|weak]
                   [--impl ours|reference]
 
 A "step" is one full timestep of the hot path (prep -> fused micro kernel ->
@@ -82,6 +82,11 @@ def make_workload(name, n_gpus=1, px=1, py=1):
         v, faces, eps, ic = (-8.0, 8.0), "walls", 5e-2, "bump"
         wl = "C4 closed box, diffuse walls, 1024^2 x 32^2, eps=5e-2"
         Lx = Ly = 1.0
+    elif name == "c4s":
+        nx = ny = 1024
+        v, faces, eps, ic = (-8.0, 8.0), "specular", 5e-2, "bump"
+        wl = "C4 closed box, specular walls (BASELINE wording), 1024^2 x 32^2, eps=5e-2"
+        Lx = Ly = 1.0
     elif name == "c5":
         nx = ny = 2048
         v, faces, eps, ic = (-7.0, 7.0), "periodic", 1e-2, "fourier"
@@ -100,6 +105,8 @@ def make_workload(name, n_gpus=1, px=1, py=1):
         bc = mm.BoundarySpec2D(mm.PERIODIC, mm.PERIODIC, mm.PERIODIC, mm.PERIODIC)
     elif faces == "extrapolate":
         bc = mm.BoundarySpec2D(mm.EXTRAPOLATE, mm.EXTRAPOLATE, mm.EXTRAPOLATE, mm.EXTRAPOLATE)
+    elif faces == "specular":
+        bc = mm.BoundarySpec2D(mm.SPECULAR, mm.SPECULAR, mm.SPECULAR, mm.SPECULAR)
     else:
         w = mm.WallSpec(1.0, 0.0)
         bc = mm.BoundarySpec2D(w, w, w, w)
