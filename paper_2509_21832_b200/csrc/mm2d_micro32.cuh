@@ -233,8 +233,10 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
 }
 
 // build the per-cell tables from the shared copy P of the cell's CellPar.
-// Warp 0 the K-table, warp 1 the L-table and the cross-term table, warp 2
-// the Gaussian GA / GD, warp 3 GB.  The closed-form target polynomial is
+// Warp 0 (which does not reduce) the K-table's Maxwellian factor and the
+// target coefficients it scales, warp 1 the L-table, warp 2 the Gaussian GA
+// and the cross-term table, warp 3 the exp-free K-table pairs and the
+// Gaussian GB and GD: the six exps per cell spread 1 / 1 / 2 / 2.  The closed-form target polynomial is
 // stored pre-scaled by mtw = -wh/tau with the Gaussian's -M wh/eps folded
 // into U.  As a polynomial in W2 the bracket is f0(k) + f1(k) W2 + f2(k) W2^2
 // + f3 W2^3 (f3 cell-constant), so with the Maxwellian's factors folded in the
@@ -250,19 +252,12 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
     if (t < 32) {
         const double W1 = v1s[m] - P.u1;
         const double W1s = W1 * W1;
-        const double w1 = W1 * P.isT;
-        const double h1 = 0.5 * w1 * w1 - 1.0;
         const double q1 = W1s * P.inv2T - 2.0;
         const double p1 = W1 * P.gT1 * P.invT;
         const double U = W1s * P.s11 * P.inv2T + q1 * p1;
         const double pe = P.pref * fexp(-W1s * P.inv2T, etab);
-        // the x-stage upwind coefficient (sign folded: v1 < 0 exactly for k < 16)
-        const double cxm = (m < NV / 2 ? -a.dt : a.dt) * v1s[m] * a.idx;
         double* K = T + KT + KW * m;
-        sts2(K + K_W1N, w1, h1);
         sts2(K + K_PE1, pe, W1);
-        sts2(K + K_XW, cxm * w1, cxm * h1);
-        sts2(K + K_W12, W1s, W1s * W1);
         // bracket U + V + c W2 + q1 p2 + p1 q2 (_core.pyx:220-224) by powers of W2:
         // f0 = U, f1 = (W1 s12 + q1 gT2) / T, f2 = (p1 - s11) / (2T), f3 = gT2 / (2T^2)
         sts2(K + K_F0, pe * fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
@@ -286,29 +281,40 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         L[L_EW1 * NV] = E2 * W2;
         L[L_EW2 * NV] = E2 * W2s;
         L[L_EW3 * NV] = (mtw * (P.gT2 * P.invT * P.inv2T)) * (E2 * (W2s * W2));
-        if (gauss) {
-            // lanes 0-15: X0 at l = 2m; lanes 16-31: R and its powers at l = 2(m-16)
-            const int lp = m & 15;
-            const double W2e = v2s[2 * lp] - P.u2;
-            const double x = fexp(P.gq12 * (m < 16 ? v1s[0] - P.u1 : v1s[1] - v1s[0]) * W2e, etab);
-            double* X = T + XT + 4 * lp;
-            if (m < 16) {
-                X[X_X0] = x;
-            } else {
-                const double r2 = x * x, r4 = r2 * r2;
-                X[X_R1] = x;
-                X[X_R2] = r2;
-                X[X_R4] = r4;
-                T[XT + X_R8 + lp] = r4 * r4;
-            }
-        }
     } else if (gauss && t < 96) {
         const double W1 = v1s[m] - P.u1;
-        sts2(T + GK + 2 * m, P.gpref * a.inveps * P.wh * fexp(P.gq11 * (W1 * W1), etab),
-             fexp(P.gq12 * W1 * (v2s[1] - v2s[0]), etab));
-    } else if (gauss) {
-        const double W2 = v2s[m] - P.u2;
-        T[GL + m] = fexp(P.gq22 * (W2 * W2), etab);
+        T[GK + 2 * m] = P.gpref * a.inveps * P.wh * fexp(P.gq11 * (W1 * W1), etab);   // GA'
+        // lanes 0-15: X0 at l = 2m; lanes 16-31: R and its powers at l = 2(m-16)
+        const int lp = m & 15;
+        const double W2e = v2s[2 * lp] - P.u2;
+        const double x = fexp(P.gq12 * (m < 16 ? v1s[0] - P.u1 : v1s[1] - v1s[0]) * W2e, etab);
+        double* X = T + XT + 4 * lp;
+        if (m < 16) {
+            X[X_X0] = x;
+        } else {
+            const double r2 = x * x, r4 = r2 * r2;
+            X[X_R1] = x;
+            X[X_R2] = r2;
+            X[X_R4] = r4;
+            T[XT + X_R8 + lp] = r4 * r4;
+        }
+    } else {
+        // the exp-free K-table pairs (off warp 0's critical path)
+        const double W1 = v1s[m] - P.u1;
+        const double W1s = W1 * W1;
+        const double w1 = W1 * P.isT;
+        const double h1 = 0.5 * w1 * w1 - 1.0;
+        // the x-stage upwind coefficient (sign folded: v1 < 0 exactly for k < 16)
+        const double cxm = (m < NV / 2 ? -a.dt : a.dt) * v1s[m] * a.idx;
+        double* K = T + KT + KW * m;
+        sts2(K + K_W1N, w1, h1);
+        sts2(K + K_XW, cxm * w1, cxm * h1);
+        sts2(K + K_W12, W1s, W1s * W1);
+        if (gauss) {
+            const double W2 = v2s[m] - P.u2;
+            T[GL + m] = fexp(P.gq22 * (W2 * W2), etab);                              // GB
+            T[GK + 2 * m + 1] = fexp(P.gq12 * W1 * (v2s[1] - v2s[0]), etab);         // GD
+        }
     }
 }
 
