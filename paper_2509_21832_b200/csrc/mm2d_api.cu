@@ -392,10 +392,9 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     ctx->last_Qout = Qout;
     if (phases & 1) {
     MARK(0);
-    k_fill_qring<<<grid_for(ring, 256), 256, 0, s>>>(g, Q, ctx->d_Qr, ctx->d_err);
-    MARK(1);
+    MARK(1);   // (the Q ring is filled by k_prep)
     PrepArgs pa;
-    pa.g = g; pa.Qr = ctx->d_Qr; pa.P = ctx->d_P; pa.err = ctx->d_err; pa.iso = ctx->d_err + 1;
+    pa.g = g; pa.Q = Q; pa.Qr = ctx->d_Qr; pa.P = ctx->d_P; pa.err = ctx->d_err; pa.iso = ctx->d_err + 1;
     pa.dt = dt; pa.eps = c.eps; pa.nu = c.nu;
     {
         const double h1 = (c.v1_max - c.v1_min) / c.nv1, h2 = (c.v2_max - c.v2_min) / c.nv2;
@@ -436,11 +435,10 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
         CK(cudaLaunchKernel(ctx->micro_fn, grid, dim3(ctx->NT), args, ctx->smem, s));
     }
     MARK(3);
-    nl += 3;
-    }   // phase 0: ring, prep, micro
+    nl += 2;
+    }   // phase 0: prep (with the Q ring), micro
     if (phases & 2) {
-    k_fill_hring<<<grid_for(ring, 256), 256, 0, s>>>(g, ctx->d_Hr);
-    MARK(4);
+    MARK(4);   // (heat ghosts are resolved inside the sweeps)
     MacroArgs mc;
     mc.g = g; mc.Qr = ctx->d_Qr; mc.Hr = ctx->d_Hr; mc.Qx = ctx->d_Qx; mc.Qout = Qout;
     mc.qsrc = qsrc; mc.err = ctx->d_err; mc.dt = dt; mc.eps = c.eps; mc.nu = c.nu;
@@ -451,9 +449,9 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     MARK(5);
     k_macro_y<<<grid_for((long long)g.bx * g.by, 128), 128, 0, s>>>(mc);
     MARK(6);
-    nl += 3;
+    nl += 2;
     MARK(7);   // (the SoA heat output is written by k_macro_y)
-    }   // phase 1: heat ring, macro
+    }   // phase 1: macro sweeps
 #undef MARK
     CK(cudaGetLastError());
     if (phases == 3) ctx->launches_per_step = nl;

@@ -161,10 +161,12 @@ __global__ void k_macro_x(MacroArgs a) {
             const double Fp = (0.0 + Lc[m]) + Rr[m];
             o[m] = qc[m] - a.rx * (Fp - Fm);
         }
-        // heat: interface means of H111, H112, H122 (x-sweep sources)
-        const double* hc = a.Hr + 4 * ring_index(g, i, j);
-        const double* hl = a.Hr + 4 * ring_index(g, i - 1, j);
-        const double* hr = a.Hr + 4 * ring_index(g, i + 1, j);
+        // heat: interface means of H111, H112, H122 (x-sweep sources); ghost
+        // cells resolved on the fly (interface_heat_2d rules)
+        double hc[4], hl[4], hr[4];
+        load_ring_h(g, a.Hr, i, j, hc);
+        load_ring_h(g, a.Hr, i - 1, j, hl);
+        load_ring_h(g, a.Hr, i + 1, j, hr);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const double hp = 0.5 * (hr[c] + hc[c]);
@@ -219,8 +221,9 @@ __global__ void k_macro_y(MacroArgs a) {
             q3[m] = qc[m] - a.ry * (Fp - Fm);
         }
         const double* hc = a.Hr + 4 * ring_index(g, i, j);
-        const double* hd = a.Hr + 4 * ring_index(g, i, j - 1);
-        const double* hu = a.Hr + 4 * ring_index(g, i, j + 1);
+        double hd[4], hu[4];
+        load_ring_h(g, a.Hr, i, j - 1, hd);
+        load_ring_h(g, a.Hr, i, j + 1, hu);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const double hp = 0.5 * (hu[c + 1] + hc[c + 1]);

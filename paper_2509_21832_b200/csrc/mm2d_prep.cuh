@@ -55,6 +55,30 @@ __device__ __forceinline__ double h_mirror_sign(int c, int flip) {
     return odd ? -1.0 : 1.0;
 }
 
+// Conserved state of ring cell (i, j) resolved from the owned block Q or a
+// received halo cell of the ring (never a cell this step writes), with the
+// specular signs applied.  Returns false if (i, j) is itself a received cell.
+__device__ __forceinline__ bool load_ring_q(const Geometry& g, const double* __restrict__ Q,
+                                            const double* Qr, int i, int j, double* q) {
+    int si, sj, flip;
+    const int rs = resolve_ring(g.bx, g.by, g.qxlo, g.qxhi, g.qylo, g.qyhi, i, j, si, sj, flip);
+    const double* src;
+    bool own_copy = true;
+    if (rs == RS_INTERIOR) {
+        src = Q + 6 * ((size_t)si * g.by + sj);
+    } else if (rs == RS_RING) {
+        src = Qr + 6 * ring_index(g, si, sj);
+        own_copy = !(si == i && sj == j);
+    } else {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) q[c] = 0.0;
+        return true;
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) q[c] = flip ? q_mirror_sign(c, flip) * src[c] : src[c];
+    return own_copy;
+}
+
 // Fill the ghost ring of Qr from the owned block Q (bx, by, 6).  Cells that
 // resolve to themselves as received halo data are left untouched.
 __global__ void k_fill_qring(Geometry g, const double* __restrict__ Q, double* __restrict__ Qr,
@@ -106,9 +130,27 @@ __global__ void k_fill_hring(Geometry g, double* __restrict__ Hr) {
     }
 }
 
+// Heat tensor of ring cell (i, j): owned and received cells from the ring,
+// ghosts resolved on the fly (wrap / copy / zero / specular image), which is
+// what the ring fill k_fill_hring stores.
+__device__ __forceinline__ void load_ring_h(const Geometry& g, const double* Hr, int i, int j,
+                                            double* h) {
+    int si, sj, flip;
+    const int rs = resolve_ring(g.bx, g.by, g.hxlo, g.hxhi, g.hylo, g.hyhi, i, j, si, sj, flip);
+    if (rs == RS_ZERO) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) h[c] = 0.0;
+        return;
+    }
+    const double* src = Hr + 4 * ring_index(g, si, sj);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) h[c] = flip ? h_mirror_sign(c, flip) * src[c] : src[c];
+}
+
 struct PrepArgs {
     Geometry g;
-    const double* Qr;
+    const double* Q;              // owned block (bx, by, 6)
+    double* Qr;                   // ring, written here (received halo cells kept)
     CellPar* P;
     unsigned long long* err;      // sticky error key
     unsigned long long* iso;      // [4]: max|m11-T|, max|m12|, max|m22-T|, max T (bit patterns)
@@ -175,7 +217,13 @@ __global__ void k_prep(PrepArgs a) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
         const bool own = i >= 0 && i < g.bx && j >= 0 && j < g.by;
-        const double* q = a.Qr + 6 * t;
+        // the ring fill (extract_ring rules) fused in: this cell's state from
+        // Q / a received halo cell, written to the ring for the macro sweeps
+        double q[6];
+        if (load_ring_q(g, a.Q, a.Qr, i, j, q)) {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) a.Qr[6 * t + c] = q[c];
+        }
         CellPar P;
         double rho, u1, u2, t11, t12, t22;
         rho = q[0];
@@ -239,11 +287,12 @@ __global__ void k_prep(PrepArgs a) {
             double r_, xu1[2], xu2[2], xT[2], yu1[2], yu2[2], yT[2];
             double a11, a12, a22;
             for (int s = 0; s < 2; ++s) {
-                const double* qx = a.Qr + 6 * ring_index(g, i + (s ? 1 : -1), j);
-                prims_fast(qx, r_, xu1[s], xu2[s], a11, a12, a22);
+                double qn[6];
+                load_ring_q(g, a.Q, a.Qr, i + (s ? 1 : -1), j, qn);
+                prims_fast(qn, r_, xu1[s], xu2[s], a11, a12, a22);
                 xT[s] = 0.5 * (a11 + a22);
-                const double* qy = a.Qr + 6 * ring_index(g, i, j + (s ? 1 : -1));
-                prims_fast(qy, r_, yu1[s], yu2[s], a11, a12, a22);
+                load_ring_q(g, a.Q, a.Qr, i, j + (s ? 1 : -1), qn);
+                prims_fast(qn, r_, yu1[s], yu2[s], a11, a12, a22);
                 yT[s] = 0.5 * (a11 + a22);
             }
             const double du1x = (xu1[1] - xu1[0]) * a.h2x;
