@@ -445,9 +445,13 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     mc.rx = dt / g.dx; mc.ry = dt / g.dy; mc.tau_kind = c.tau_kind; mc.tau_value = c.tau_value;
     mc.step = 0;
     mc.Hout = H;
-    k_macro_x<<<grid_for((long long)g.bx * (g.by + 2), 128), 128, 0, s>>>(mc);
+    {
+        const int jlo = g.qylo == GM_HALO ? -1 : 0, jhi = g.qyhi == GM_HALO ? g.by : g.by - 1;
+        dim3 gx((g.bx + MX_TI - 1) / MX_TI, (jhi - jlo + 1 + MX_TJ - 1) / MX_TJ);
+        k_macro_x<<<gx, dim3(MX_TJ, MX_TI + 2), 0, s>>>(mc);
+    }
     MARK(5);
-    k_macro_y<<<grid_for((long long)g.bx * g.by, 128), 128, 0, s>>>(mc);
+    k_macro_y<<<dim3((g.by + MY_OUT - 1) / MY_OUT, (g.bx + 3) / 4), 128, 0, s>>>(mc);
     MARK(6);
     nl += 2;
     MARK(7);   // (the SoA heat output is written by k_macro_y)

@@ -51,10 +51,10 @@ constexpr int GL = GK + 2 * NV;      // Gaussian l-table [32] (GB)
 constexpr int XT = GL + NV;          // Gaussian cross-term table [16][4] per even l + R^8 [16]
 constexpr int TAB = XT + 5 * 16;     // 816 doubles per cell
 // K-table pairs (16-byte loads): (w1, h1) (pE1, W1) (cx w1, cx h1) (W1^2, W1^3)
-// (pE1 f0, pE1 f1) (pE1 f2, -) -- the target polynomial's W2-power
+// (pE1 f0, pE1 f1) (pE1 f2, pE1) -- the target polynomial's W2-power
 // coefficients pre-multiplied by the Maxwellian's k factor, the x-sum weights
 // by the upwind coefficient
-enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_W12, K_W13, K_F0, K_F1, K_F2, K_F2PAD };
+enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_W12, K_W13, K_F0, K_F1, K_F2, K_PE1B };
 // L-table rows: E2, w2, h2, W2, E2 W2, E2 W2^2, f3 E2 W2^3
 enum { L_E2, L_W2N, L_H2, L_W2, L_EW1, L_EW2, L_EW3, L_PAD };
 // cross-term table per even l = 2 lp: X0 = exp(q12 W1_0 W2), R = exp(q12 dv1 W2),
@@ -262,7 +262,7 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         // f0 = U, f1 = (W1 s12 + q1 gT2) / T, f2 = (p1 - s11) / (2T), f3 = gT2 / (2T^2)
         sts2(K + K_F0, pe * fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
              pe * (mtw * ((W1 * P.s12 + q1 * P.gT2) * P.invT)));
-        sts2(K + K_F2, pe * (mtw * ((p1 - P.s11) * P.inv2T)), 0.0);
+        sts2(K + K_F2, pe * (mtw * ((p1 - P.s11) * P.inv2T)), pe);   // pE1 again: one 16-byte load in the target
         if (m == 0) {
             sts2(T + HD + H_SCALE, P.scale, P.wg);
             sts2(T + HD + H_MTW, mtw, a.inveps * P.wh);
@@ -841,11 +841,11 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
 #pragma unroll
                 for (int p = 0; p < NP_; ++p) {
                     const double* K = T + koff_(p);
-                    const double pe = K[K_PE1];
                     // closed-form target (_core.pyx:220-224), factored and
                     // pre-scaled by -wh/tau (minus wh/eps when Gaussian)
                     const double2 f01 = lds2(K + K_F0);   // pe f0', pe f1'
-                    const double f2 = K[K_F2];             // pe f2'
+                    const double2 f2p = lds2(K + K_F2);   // pe f2', pe
+                    const double f2 = f2p.x, pe = f2p.y;
                     double P0 = fma(wg, ty[2 * p], f01.x * E2.x);
                     double P1 = fma(wg, ty[2 * p + 1], f01.x * E2.y);
                     P0 = fma(f01.y, e1.x, P0); P1 = fma(f01.y, e1.y, P1);
