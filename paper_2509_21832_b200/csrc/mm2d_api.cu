@@ -258,12 +258,12 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->dev);
         // Band height: a CTA walks one column through ly rows, paying ~4
         // pipeline-fill iterations per band.  Measured on C2 (256 x 256,
-        // 148 SMs x 3 CTAs, kernel v16): ly 48 / 50 / 52 / 54 / 56 / 58 / 60 / 64
-        // give 0.412 / 0.411 / 0.415 / 0.411 / 0.407 / 0.411 / 0.416 / 0.424 ms;
-        // a wave-quantisation model (minimise waves * (ly + 4)) predicts 52
-        // and is not borne out, so the measured optimum is the default.
+        // 148 SMs x 4 CTAs, kernel v18): ly 32 / 40 / 43 / 48 / 56 / 64 / 86 / 128
+        // give 0.412 / 0.398 / 0.409 / 0.410 / 0.409 / 0.390 / 0.438 / 0.419 ms
+        // (partial-wave effects dominate at 256 columns); at C4 (1024^2) 64
+        // and 56 give 5.47 and 5.51 ms.
         const char* ly = getenv("MM2D_LY");
-        ctx->ly32 = ly ? std::max(1, atoi(ly)) : 56;
+        ctx->ly32 = ly ? std::max(1, atoi(ly)) : 64;
         ctx->ly32 = std::min(ctx->ly32, g.by);
         const long long items = (long long)((g.by + ctx->ly32 - 1) / ctx->ly32) * g.bx;
         const char* pe = getenv("MM2D_PERSIST");

@@ -29,9 +29,10 @@
 #include "mm2d_micro.cuh"
 
 #ifndef MICRO32_MINB
-#define MICRO32_MINB 3   // resident CTAs per SM the register budget is sized for (4 fits
-                         // the 52 KB of shared memory but spills at 128 registers and is
-                         // 11% slower)
+#define MICRO32_MINB 4   // resident CTAs per SM the register budget is sized for: 4 x 128
+                         // threads at 128 registers and 55 KB of shared memory (the K-table
+                         // drops its W1^2 / W1^3 pair to fit).  Measured against 3 CTAs at
+                         // 166 registers: C4 5.47 vs 5.84 ms, C2 (band 64) 0.390 vs 0.405 ms.
 #endif
 
 namespace mm2d {
@@ -43,7 +44,13 @@ constexpr int NT = 128;              // threads of the default 8-node (NP = 4) v
 constexpr int NP = 4;                // node pairs per thread (default variant)
 constexpr int TSLOTS = 4;            // table slots (rows j..j+3; the slot rebuilt
                                      // at iteration j last held row j-1)
+#if MICRO32_MINB >= 4
+#define M32_W1POW_TABLE 0            // 4 CTAs/SM: recompute W1^2, W1^3 to fit 56 KB
+constexpr int KW = 10;               // K-table entries per k
+#else
+#define M32_W1POW_TABLE 1
 constexpr int KW = 12;               // K-table entries per k
+#endif
 constexpr int KT = 0;                // K-table [32][KW]
 constexpr int LT = KT + KW * NV;     // L-table [8][32]
 constexpr int GK = LT + 8 * NV;      // Gaussian k-table [32][2] (GA, GD)
@@ -54,7 +61,11 @@ constexpr int TAB = XT + 5 * 16;     // 816 doubles per cell
 // (pE1 f0, pE1 f1) (pE1 f2, pE1) -- the target polynomial's W2-power
 // coefficients pre-multiplied by the Maxwellian's k factor, the x-sum weights
 // by the upwind coefficient
+#if M32_W1POW_TABLE
 enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_W12, K_W13, K_F0, K_F1, K_F2, K_PE1B };
+#else
+enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_F0, K_F1, K_F2, K_PE1B };
+#endif
 // L-table rows: E2, w2, h2, W2, E2 W2, E2 W2^2, f3 E2 W2^3
 enum { L_E2, L_W2N, L_H2, L_W2, L_EW1, L_EW2, L_EW3, L_PAD };
 // cross-term table per even l = 2 lp: X0 = exp(q12 W1_0 W2), R = exp(q12 dv1 W2),
@@ -309,7 +320,9 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         double* K = T + KT + KW * m;
         sts2(K + K_W1N, w1, h1);
         sts2(K + K_XW, cxm * w1, cxm * h1);
+#if M32_W1POW_TABLE
         sts2(K + K_W12, W1s, W1s * W1);
+#endif
         if (gauss) {
             const double W2 = v2s[m] - P.u2;
             T[GL + m] = fexp(P.gq22 * (W2 * W2), etab);                              // GB
@@ -900,7 +913,13 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 const double* K = T + koff_(p);
                 const double2 wh = lds2(K + K_W1N);     // w1, h1
                 const double2 pw = lds2(K + K_PE1);     // pE1, W1
+#if M32_W1POW_TABLE
                 const double2 w3 = lds2(K + K_W12);     // W1^2, W1^3
+#else
+                double2 w3;
+                w3.x = pw.y * pw.y;
+                w3.y = w3.x * pw.y;
+#endif
                 const double alp = fma(wh.x, a2, fma(wh.y, a4, a1)) * pw.x;
                 const double o0 = fma(alp, E2.x, fma(bE0, pw.x, acc[2 * p]));
                 const double o1 = fma(alp, E2.y, fma(bE1, pw.x, acc[2 * p + 1]));
