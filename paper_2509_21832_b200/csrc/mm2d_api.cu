@@ -46,6 +46,7 @@ struct mm2d_ctx {
     double* d_zero = nullptr;      // V zeros
     bool use32 = false;            // specialised 32 x 32 micro kernel
     int grid32 = 1;                // persistent CTAs of k_micro32
+    std::vector<int> bands32;      // non-uniform band boundaries (empty: uniform ly32)
     int np32 = 4;                  // node pairs per thread of k_micro32
     int ly32 = 32;
     // context-owned state
@@ -114,6 +115,41 @@ static int ghost_mode(const mm2d_config& c, int face, bool at_edge, int nranks_a
     if (kind == MM2D_FACE_EXTRAPOLATE) return GM_COPY;
     if (kind == MM2D_FACE_SPECULAR) return GM_MIRROR;
     return field == 1 ? GM_COPY : GM_ZERO;
+}
+
+// Band layout for k_micro32 when the block is too small for uniform bands
+// to fill the resident CTA slots in whole waves (C2: 256 columns, 592
+// slots).  Every column gets L long bands of H rows plus one short band of
+// R = by - L H rows; the L bx long CTAs take one slot each for H + 4 row
+// times (4 = the row pipeline's fill) while the spare slots run the bx short
+// CTAs back to back, so H is the smallest height at which
+//     spare (H + 4) >= bx (R + 4),   spare = slots - L bx.
+// All columns share the band boundaries, so neighbouring columns still run
+// the same rows together (the x-halo halves stay in L2).  Chosen over
+// uniform bands of `ly` rows (makespan ~ waves (ly + 4)) when it is at
+// least 3% shorter.  Measured at C2: uniform 64 -> 0.391 ms, [112,112,32]
+// -> 0.377 ms; [114,114,28] 0.377, [116,116,24] 0.383, [108,108,40] 0.392.
+static std::vector<int> pick_bands(int bx, int by, long long slots, int ly) {
+    const long long ov = 4;
+    const long long nb = (by + ly - 1) / ly;
+    const long long waves = ((long long)bx * nb + slots - 1) / slots;
+    double best = (double)waves * (ly + ov);
+    std::vector<int> out;
+    for (int L = 1; L <= 8 && (long long)L * bx < slots; ++L) {
+        const long long spare = slots - (long long)L * bx;
+        const long long num = (long long)bx * (by + ov) - ov * spare;
+        const long long den = spare + (long long)L * bx;
+        const long long H = (num + den - 1) / den;
+        const long long R = by - L * H;
+        if (H < 16 || R < 1 || R >= H) continue;
+        if ((double)(H + ov) < 0.97 * best) {
+            best = (double)(H + ov);
+            out.assign(1, 0);
+            for (int b = 1; b <= L; ++b) out.push_back((int)(b * H));
+            out.push_back(by);
+        }
+    }
+    return out;
 }
 
 extern "C" int mm2d_version(void) { return 1; }
@@ -264,7 +300,38 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         // and 56 give 5.47 and 5.51 ms.
         const char* ly = getenv("MM2D_LY");
         ctx->ly32 = ly ? std::max(1, atoi(ly)) : 64;
+        // explicit band heights (same for every column), e.g. MM2D_BANDS=114,114,22,6
+        if (const char* bs = getenv("MM2D_BANDS")) {
+            std::vector<int> h;
+            for (const char* q = bs; *q;) {
+                h.push_back(atoi(q));
+                while (*q && *q != ',') ++q;
+                if (*q == ',') ++q;
+            }
+            int acc = 0;
+            ctx->bands32.push_back(0);
+            for (int x : h) {
+                if (x <= 0 || (int)ctx->bands32.size() > 8) break;
+                acc = std::min(g.by, acc + x);
+                ctx->bands32.push_back(acc);
+                if (acc == g.by) break;
+            }
+            if (ctx->bands32.back() != g.by) ctx->bands32.clear();   // must cover the block
+        } else if (!ly) {
+            ctx->bands32 = pick_bands(g.bx, g.by, (long long)std::max(occ, 1) * std::max(nsm, 1),
+                                      ctx->ly32);
+        }
         ctx->ly32 = std::min(ctx->ly32, g.by);
+        if (getenv("MM2D_VERBOSE")) {
+            fprintf(stderr, "mm2d: k_micro32 %d CTAs/SM x %d SMs, block %d x %d, bands", occ, nsm,
+                    g.bx, g.by);
+            if (ctx->bands32.empty()) fprintf(stderr, " uniform %d\n", ctx->ly32);
+            else {
+                for (size_t b = 1; b < ctx->bands32.size(); ++b)
+                    fprintf(stderr, " %d", ctx->bands32[b] - ctx->bands32[b - 1]);
+                fprintf(stderr, "\n");
+            }
+        }
         const long long items = (long long)((g.by + ctx->ly32 - 1) / ctx->ly32) * g.bx;
         const char* pe = getenv("MM2D_PERSIST");
         const bool persist = pe ? atoi(pe) != 0 : false;
@@ -428,6 +495,11 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
         }
         ma.ly = ctx->ly32;
         dim3 grid(g.bx, (g.by + ctx->ly32 - 1) / ctx->ly32);
+        if (!ctx->bands32.empty()) {
+            ma.nband = (int)ctx->bands32.size() - 1;
+            for (int b = 0; b <= ma.nband; ++b) ma.band_j0[b] = ctx->bands32[b];
+            grid.y = ma.nband;
+        }
         m32::launch_micro32(ma, grid, s);
     } else {
         dim3 grid((g.bx + ctx->BX - 1) / ctx->BX, (g.by + ctx->ly - 1) / ctx->ly);

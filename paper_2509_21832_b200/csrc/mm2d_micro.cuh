@@ -48,6 +48,8 @@ struct MicroArgs {
     const double* wall_ghat;  // precomputed wall-strip targets (k_wall_ghat)
     const double* zero;       // V zeros (zero ghosts of the specialised kernel)
     int ly;                   // rows per segment
+    int nband;                // k_micro32: 0 = uniform bands of ly rows, else band
+    int band_j0[9];           //   b covers rows [band_j0[b], band_j0[b+1]) (all columns)
     int gauss;                // nu != 0
     double dt, eps, inveps, idx, idy, dv, hfac;  // hfac = eps * dv
 };

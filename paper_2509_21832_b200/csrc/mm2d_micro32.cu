@@ -1,4 +1,5 @@
 // Translation unit of the 32 x 32 fused micro kernel (mm2d_micro32.cuh).
+#include <algorithm>
 #include "mm2d_micro32.cuh"
 #include "mm2d_micro32_launch.h"
 
@@ -13,8 +14,26 @@ cudaError_t setup(int* ctas_per_sm) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sm);
         if (e != cudaSuccess) return e;
+        // all of the unified L1 as shared memory: 4 CTAs x 55 KB per SM (the
+        // occupancy query below reports 1 CTA/SM under the default carveout)
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
     }
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, fns[0], 128, sm);
+    // resident CTAs per SM from the kernel's registers and shared memory (the
+    // runtime's occupancy query reports 1 for this kernel, while 4 run)
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, fns[0]);
+    if (e != cudaSuccess) return e;
+    int dev = 0, regs_sm = 0, smem_sm = 0, rsv = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    const int by_regs = regs_sm / std::max(1, fa.numRegs * 128);
+    const int by_smem = smem_sm / (int)(sm + fa.sharedSizeBytes + rsv);
+    *ctas_per_sm = std::max(1, std::min(by_regs, by_smem));
+    return cudaSuccess;
 }
 
 void launch_micro32(const MicroArgs& a, dim3 grid, cudaStream_t s) {

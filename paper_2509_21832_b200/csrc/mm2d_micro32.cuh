@@ -545,8 +545,8 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     const size_t V_ = V;
 
     const int i = blockIdx.x;
-    const int j0s = blockIdx.y * a.ly;
-    const int j1s = min(g.by, j0s + a.ly);
+    const int j0s = a.nband ? a.band_j0[blockIdx.y] : blockIdx.y * a.ly;
+    const int j1s = a.nband ? a.band_j0[blockIdx.y + 1] : min(g.by, j0s + a.ly);
     const int k_lo = row_kind(g, j0s - 1);          // ghost-row kinds at the piece ends
     const int k_hi = row_kind(g, j1s);
 
