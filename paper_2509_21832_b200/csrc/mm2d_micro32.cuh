@@ -841,15 +841,21 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 // ES-BGK Gaussian GA GB X with X(k, l) = exp(q12 W1 W2): the
                 // thread's base X0 R^kb from the cross-term table, then R^8 per pair
                 double2 GB = make_double2(0.0, 0.0);
-                double GR = 1.0, Xp = 0.0;
+                double Xq[NP_];            // X(k, lb) of the thread's pairs, as a product tree
+#pragma unroll
+                for (int p = 0; p < NP_; ++p) Xq[p] = 0.0;
                 if (gauss) {
                     GB = lds2(T + GL + lb);
                     const double2 x0 = lds2(T + XT + xsel + X_X0);   // X0, R
                     const double2 r24 = lds2(T + XT + xsel + X_R2);  // R^2, R^4
-                    GR = T[XT + X_R8 + lp];
-                    Xp = x0.x * ((kb & 1) ? x0.y : 1.0);
-                    Xp *= (kb & 2) ? r24.x : 1.0;
-                    Xp *= (kb & 4) ? r24.y : 1.0;
+                    const double r8 = T[XT + X_R8 + lp];
+                    const double xb = (x0.x * ((kb & 1) ? x0.y : 1.0)) *
+                                      (((kb & 2) ? r24.x : 1.0) * ((kb & 4) ? r24.y : 1.0));
+                    const double r16 = r8 * r8;
+                    Xq[0] = xb;
+                    Xq[1] = xb * r8;
+                    Xq[2] = xb * r16;
+                    Xq[3] = xb * (r16 * r8);
                 }
 #pragma unroll
                 for (int p = 0; p < NP_; ++p) {
@@ -867,10 +873,9 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                     if (gauss) {
                         // + Gaussian wh/eps, Gaussian = GA GB X
                         const double2 gad = lds2(T + GK + 2 * (kb + KS * p));   // GA', GD
-                        const double Y0 = gad.x * Xp;
+                        const double Y0 = gad.x * Xq[p];
                         P0 = fma(GB.x, Y0, P0);
                         P1 = fma(GB.y, Y0 * gad.y, P1);
-                        Xp *= GR;
                     }
                     acc[2 * p] = P0;
                     acc[2 * p + 1] = P1;
