@@ -300,3 +300,34 @@ def test_v1024_degenerate_grids_vs_oracle(mm, oracle, shape, faces_kind):
     # a lone periodic cell relaxes G to ~1e-6, pure roundoff of the O(0.1)
     # Maxwellian terms: compare G on a 1e-4 floor
     assert rel_err(st.G, Go, floor=1e-4) <= TOL_G
+
+
+# -- band layouts of the 32 x 32 kernel (mm2d_api.cu pick_bands) ----------
+
+@pytest.mark.parametrize("bands", ["auto", "7,20,5", "1,1,30", "32", "3,3,3,3,3,3,3,11"])
+def test_v1024_band_layout_is_bitwise_neutral(mm, bands, monkeypatch):
+    """The specialised kernel walks each column in bands of rows; the layout
+    (uniform, the automatic long/short split, or explicit MM2D_BANDS) only
+    changes the schedule, never the arithmetic: results are bitwise equal."""
+    import torch
+    from paper_2509_21832_b200 import PERIODIC, WallSpec
+    from paper_2509_21832_b200.solver import Solver2D
+    w = WallSpec(1.0)
+    mesh, bc, eps, model, Q, G, dt = _random_problem(mm, 9, 32, 32, (w, w, PERIODIC, PERIODIC),
+                                                     -0.5, 0.05, 5)
+    outs = []
+    for env in ({"MM2D_LY": "32"}, {} if bands == "auto" else {"MM2D_BANDS": bands}):
+        for k in ("MM2D_LY", "MM2D_BANDS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = Solver2D(mesh, bc, eps, model)
+        Qd = torch.from_numpy(Q).cuda()
+        Gd = torch.from_numpy(G).cuda()
+        for _ in range(3):
+            Qd, Gd, Hd = s.step(Qd, Gd, dt)
+        torch.cuda.synchronize()
+        s.check()
+        outs.append((Qd.cpu().numpy(), Gd.cpu().numpy(), Hd.cpu().numpy()))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
