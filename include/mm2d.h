@@ -114,7 +114,11 @@ int mm2d_step(mm2d_ctx *ctx, const double *d_Q, const double *d_G, double dt,
  * decomposition (parallel.py:384-394): phase 0 = macro ring + per-cell prep
  * + fused micro kernel (writes G^{n+1} and the owned heat tensor), phase 1 =
  * heat ring + KFVS/TR-BDF2 macro update.  Between them a multi-rank run
- * exchanges the heat-tensor halo (mm2d_halo_*, field 2). */
+ * exchanges the heat-tensor halo (mm2d_halo_*, field 2).  Phase 0 may itself
+ * be split around the G halo exchange so the exchange overlaps interior-cell
+ * compute: phase 2 = prep + the micro CTAs that read no received G halo
+ * (needs only the Q halo), phase 3 = the remaining micro CTAs (after the G
+ * halo has landed); 2 then 3 is bitwise identical to 0. */
 int mm2d_step_phase(mm2d_ctx *ctx, int phase, const double *d_Q, const double *d_G, double dt,
                     double *d_Qout, double *d_Gout, double *d_H,
                     int nsrc, const double *d_src_coeffs, const double *d_src_shapes,

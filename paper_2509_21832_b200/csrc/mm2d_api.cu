@@ -443,7 +443,7 @@ static int grid_for(long long n, int threads) {
 static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double dt, double* Qout,
                         double* Gout, double* H, int nsrc, const double* sc, const double* ss,
                         const double* qsrc, cudaStream_t s, cudaEvent_t* ev = nullptr,
-                        int phases = 3) {
+                        int phases = 3, int part = 0) {
 #define MARK(q) \
     if (ev) CK(cudaEventRecord(ev[q], s))
     const Geometry& g = ctx->g;
@@ -473,7 +473,10 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     pa.step = 0;
     pa.gauss = gauss;
     pa.h2x = 0.5 / g.dx; pa.h2y = 0.5 / g.dy;
-    k_prep<<<grid_for(ring, 128), 128, 0, s>>>(pa);
+    if (part != 2) {   // the halo part of a split micro launch reuses the prep of part 1
+        k_prep<<<grid_for(ring, 128), 128, 0, s>>>(pa);
+        ++nl;
+    }
     MARK(2);
     MicroArgs ma;
     memset(&ma, 0, sizeof(ma));
@@ -488,8 +491,9 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     ma.dv = pa.dv; ma.hfac = c.eps * pa.dv;
     ma.wall_ghat = ctx->d_wallg;
     ma.zero = ctx->d_zero;
+    ma.part = part;
     if (ctx->use32 && nsrc == 0) {
-        if (ctx->d_wallg) {
+        if (ctx->d_wallg && part != 2) {
             m32::launch_wall_ghat(ma, ctx->d_wallg, 2 * g.by + 2 * g.bx, s);
             ++nl;
         }
@@ -507,7 +511,7 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
         CK(cudaLaunchKernel(ctx->micro_fn, grid, dim3(ctx->NT), args, ctx->smem, s));
     }
     MARK(3);
-    nl += 2;
+    nl += 1;
     }   // phase 0: prep (with the Q ring), micro
     if (phases & 2) {
     MARK(4);   // (heat ghosts are resolved inside the sweeps)
@@ -539,10 +543,13 @@ extern "C" int mm2d_step_phase(mm2d_ctx* ctx, int phase, const double* d_Q, cons
                                double dt, double* d_Qout, double* d_Gout, double* d_H, int nsrc,
                                const double* d_src_coeffs, const double* d_src_shapes,
                                const double* d_qsrc, void* stream) {
-    if (!ctx || (phase != 0 && phase != 1)) return fail_cfg(ctx, "phase must be 0 or 1");
+    if (!ctx || phase < 0 || phase > 3) return fail_cfg(ctx, "phase must be 0, 1, 2 or 3");
     CK(cudaSetDevice(ctx->dev));
+    // 2 / 3: phase 0 split around the G halo exchange -- prep and the micro
+    // CTAs that read no received halo, then the CTAs that do
     return enqueue_step(ctx, d_Q, d_G, dt, d_Qout, d_Gout, d_H, nsrc, d_src_coeffs,
-                        d_src_shapes, d_qsrc, (cudaStream_t)stream, nullptr, 1 << phase);
+                        d_src_shapes, d_qsrc, (cudaStream_t)stream, nullptr,
+                        phase == 1 ? 2 : 1, phase >= 2 ? phase - 1 : 0);
 }
 
 extern "C" int mm2d_step(mm2d_ctx* ctx, const double* d_Q, const double* d_G, double dt,

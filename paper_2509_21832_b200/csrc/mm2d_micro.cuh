@@ -51,8 +51,21 @@ struct MicroArgs {
     int nband;                // k_micro32: 0 = uniform bands of ly rows, else band
     int band_j0[9];           //   b covers rows [band_j0[b], band_j0[b+1]) (all columns)
     int gauss;                // nu != 0
+    int part;                 // 0 all CTAs; 1 only CTAs that read no received G halo
+                              // (run while the halo exchange is in flight); 2 only the others
     double dt, eps, inveps, idx, idy, dv, hfac;  // hfac = eps * dv
 };
+
+// Does the CTA owning columns [i0, i1) and rows [j0, j1) read a received G
+// halo (an x halo column or a y halo row, corners included)?  Selects the
+// CTAs of each part of a split launch (MicroArgs::part).
+__device__ __forceinline__ bool reads_halo(const Geometry& g, int i0, int i1, int j0, int j1) {
+    return (i0 == 0 && g.xlo == GM_HALO) || (i1 >= g.bx && g.xhi == GM_HALO) ||
+           (j0 == 0 && g.ylo == GM_HALO) || (j1 >= g.by && g.yhi == GM_HALO);
+}
+__device__ __forceinline__ bool skip_part(const MicroArgs& a, int i0, int i1, int j0, int j1) {
+    return a.part != 0 && (reads_halo(a.g, i0, i1, j0, j1) == (a.part == 1));
+}
 
 // Pointer to G^n of ring cell (i, r) or nullptr for a zero ghost.  *mir is
 // set when the cell is the specular image (k reversed) of the returned one;
@@ -243,6 +256,7 @@ __global__ void __launch_bounds__(256) k_micro(MicroArgs a) {
     const int nb = min(BX, g.bx - ic0);              // owned cells in this strip
     const int j0s = blockIdx.y * a.ly;
     const int j1s = min(j0s + a.ly, g.by);
+    if (skip_part(a, ic0, ic0 + nb, j0s, j1s)) return;
 
     // ---- shared memory carve-up ----
     double* gstar = smem;                                         // [3][BX][V]

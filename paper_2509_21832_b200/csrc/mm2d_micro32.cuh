@@ -500,6 +500,11 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     extern __shared__ __align__(16) double smem[];
     const Geometry& g = a.g;
     if (*a.err != kNoError) return;
+    if (a.part != 0) {
+        const int b0 = a.nband ? a.band_j0[blockIdx.y] : blockIdx.y * a.ly;
+        const int b1 = a.nband ? a.band_j0[blockIdx.y + 1] : min(g.by, b0 + a.ly);
+        if (skip_part(a, blockIdx.x, blockIdx.x + 1, b0, b1)) return;
+    }
     const int tid = threadIdx.x;
     // thread -> nodes: l pair lp, k base kb.  Warps 0/2 take the v2 < 0 half
     // (l < 16), warps 1/3 the v2 >= 0 half, so the y-upwind direction is

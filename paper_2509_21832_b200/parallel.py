@@ -143,6 +143,12 @@ class DistExchange:
         return self._host[key]
 
     def exchange(self, field):
+        self.finish(self.start(field))
+
+    def start(self, field):
+        """Post the field's sends and receives; returns the handle ``finish``
+        completes.  Over NCCL the transfers run on the communicator's stream
+        while the caller keeps enqueueing work (the interior micro CTAs)."""
         import torch.distributed as dist
         ops, back = [], []
         for s in range(8):
@@ -164,9 +170,18 @@ class DistExchange:
                     back.append((recv, h))
                     recv = h
                 ops.append(dist.P2POp(dist.irecv, recv, peer, self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        if self.staged:
+            self.finish((reqs, back))
+            return ([], [])
+        return (reqs, back)
+
+    def finish(self, handle):
+        """Make the current stream wait for a started exchange (NCCL: a
+        stream-side wait, the host does not block)."""
+        reqs, back = handle
+        for req in reqs:
+            req.wait()
         for dev, h in back:
             dev.copy_(h)
 
@@ -189,6 +204,12 @@ class LoopbackExchange:
                 _, recv = self.bufs[peer][field][OPPOSITE[s]]
                 if send is not None and recv is not None:
                     recv.copy_(send, non_blocking=True)
+
+    def start(self, field):
+        self.exchange(field)
+
+    def finish(self, handle):
+        pass
 
 
 # ---------------------------------------------------------------------------
@@ -262,20 +283,32 @@ class BlockStepper:
 
 def step_blocks(blocks, exchange, states, dt):
     """One decomposed step for every block held by this process.
-    ``states[b] = (Q, G, Qout, Gout, H)`` device tensors of block b."""
+    ``states[b] = (Q, G, Qout, Gout, H)`` device tensors of block b.
+
+    The G ring exchange (V doubles per perimeter cell, the bulk of the
+    traffic) overlaps the interior cells' micro update: the Q ring (6
+    doubles per cell) is exchanged first, then the G exchange is posted, the
+    prep and every micro CTA that reads no received G halo run (phase 2),
+    and only the perimeter CTAs (phase 3) wait for the G halo.  Phases 2 + 3
+    are bitwise the unsplit phase 0."""
     import torch
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
-            b.pack(FIELD_G, st[1])
             b.pack(FIELD_Q, st[0])
+            b.pack(FIELD_G, st[1])
     _sync_devices(blocks)
-    exchange.exchange(FIELD_G)
     exchange.exchange(FIELD_Q)
     _sync_devices(blocks)
+    hg = exchange.start(FIELD_G)
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
             b.unpack(FIELD_Q)
-            b.phase(0, st[0], st[1], dt, st[2], st[3], st[4])
+            b.phase(2, st[0], st[1], dt, st[2], st[3], st[4])
+    exchange.finish(hg)
+    _sync_devices(blocks)
+    for b, st in zip(blocks, states):
+        with torch.cuda.device(b.solver.device):
+            b.phase(3, st[0], st[1], dt, st[2], st[3], st[4])
             b.pack(FIELD_H, None)
     _sync_devices(blocks)
     exchange.exchange(FIELD_H)

@@ -108,15 +108,22 @@ def _worker(rank, world, port, nx, ny, grid, faces, width, errq):
             recv = torch.full((len(cells) * width,), np.nan, dtype=torch.float64)
             row.append((send, recv))
         bufs[1] = row
-        DistExchange(p, bufs).exchange(1)
-        for s in range(8):
-            if p.slots[s] is None:
-                continue
-            ghosts = _slot_cells(p, s, ghost=True)
-            want = np.concatenate([A[i % nx, j % ny] for i, j in ghosts])
-            got = bufs[1][s][1].numpy()
-            if not np.array_equal(got, want):
-                errq.put(f"rank {rank} slot {s}: mismatch")
+        # field 0 (the G ring in the step) carries -A and goes through the
+        # split start / finish protocol step_blocks overlaps with compute
+        bufs[0] = [(None, None) if sr[0] is None else (-sr[0], sr[1].clone()) for sr in row]
+        ex = DistExchange(p, bufs)
+        ex.exchange(1)
+        h = ex.start(0)
+        ex.finish(h)
+        for f, sign in ((1, 1.0), (0, -1.0)):
+            for s in range(8):
+                if p.slots[s] is None:
+                    continue
+                ghosts = _slot_cells(p, s, ghost=True)
+                want = sign * np.concatenate([A[i % nx, j % ny] for i, j in ghosts])
+                got = bufs[f][s][1].numpy()
+                if not np.array_equal(got, want):
+                    errq.put(f"rank {rank} field {f} slot {s}: mismatch")
         dist.barrier()
         dist.destroy_process_group()
     except Exception as exc:  # pragma: no cover - surfaced through the queue
