@@ -162,3 +162,49 @@ def test_gloo_halo_exchange_matches_extract_ring(grid, faces, shape):
 
 def test_opposite_slots_are_involutions():
     assert all(OPPOSITE[OPPOSITE[s]] == s for s in range(8))
+
+
+# -- step protocol ----------------------------------------------------------
+
+def test_step_blocks_overlaps_g_exchange_with_interior_micro(monkeypatch):
+    """step_blocks' order of operations (host logic, no GPU): the Q ring is
+    exchanged first, the G exchange is posted and left in flight while the
+    prep + interior micro CTAs (phase 2) are enqueued, the perimeter CTAs
+    (phase 3) only after it completes, then the heat ring and the macro
+    phase -- the reference worker grid's two barrier points
+    (parallel.py:384-394) with the G transfer hidden behind interior work."""
+    import contextlib
+    from paper_2509_21832_b200 import parallel as par
+
+    log = []
+    monkeypatch.setattr(torch.cuda, "device", lambda d: contextlib.nullcontext())
+
+    class Blk:
+        class solver:
+            device = torch.device("cpu")
+
+        def pack(self, f, src):
+            log.append(("pack", f))
+
+        def unpack(self, f):
+            log.append(("unpack", f))
+
+        def phase(self, ph, *args):
+            log.append(("phase", ph))
+
+    class Ex:
+        def exchange(self, f):
+            log.append(("exchange", f))
+
+        def start(self, f):
+            log.append(("start", f))
+            return f
+
+        def finish(self, h):
+            log.append(("finish", h))
+
+    par.step_blocks([Blk()], Ex(), [(None,) * 5], 1e-3)
+    G, Q, H = par.FIELD_G, par.FIELD_Q, par.FIELD_H
+    assert log == [("pack", Q), ("pack", G), ("exchange", Q), ("start", G), ("unpack", Q),
+                   ("phase", 2), ("finish", G), ("phase", 3), ("pack", H), ("exchange", H),
+                   ("unpack", H), ("phase", 1)]
