@@ -14,3 +14,6 @@ python tools/profile_step.py > gpurun_out/prof_plain_$TAG.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_micro32 -s 1 -c 1 \
   -o gpurun_out/prof_$TAG python tools/profile_step.py > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu rc=$?"
 tail -2 gpurun_out/bench_$TAG.json
+for c in c3 c4 c4s c5; do
+  timeout 900 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${c}_$TAG.json 2> gpurun_out/bench_${c}_$TAG.err; echo "bench $c rc=$?"
+done
