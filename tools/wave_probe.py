@@ -1,7 +1,8 @@
-"""Micro-kernel time per node against the CTA-wave count (tail cost):
-periodic density-wave problems of different (nx, ny), ly = 48 bands.
+"""Micro-kernel time per node against the grid shape (tail and wave
+effects): periodic density-wave problems of different (nx, ny), with the
+library's own band choice (MM2D_VERBOSE=1 prints it).
 
-    python tools/wave_probe.py
+    python tools/wave_probe.py [nx,ny ...]
 """
 import ctypes as C
 import sys
@@ -17,7 +18,9 @@ import torch  # noqa: E402
 def main():
     import paper_2509_21832_b200 as mm
     from paper_2509_21832_b200.solver import Solver2D
-    for nx, ny in [(222, 288), (256, 256), (259, 288), (296, 288), (148, 480), (444, 96)]:
+    shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]] or [
+        (256, 256), (256, 1024), (1024, 256), (512, 512), (1024, 1024), (296, 256)]
+    for nx, ny in shapes:
         mesh = mm.PhaseMesh(space=(mm.Axis(0.0, 1.0, nx), mm.Axis(0.0, 1.0, ny)),
                             velocity=(mm.Axis(-7.0, 7.0, 32), mm.Axis(-7.0, 7.0, 32)))
         bc = mm.BoundarySpec2D(mm.PERIODIC, mm.PERIODIC, mm.PERIODIC, mm.PERIODIC)
@@ -36,10 +39,8 @@ def main():
         dt = 0.4 * (1.0 / nx) / 7.0
         s.lib.mm2d_time_kernels(s.ctx, C.c_double(dt), 3, ms)
         s.lib.mm2d_time_kernels(s.ctx, C.c_double(dt), 10, ms)
-        ctas = nx * ((ny + 47) // 48)
         ns = ms[2] * 1e6 / (nx * ny * 1024)
-        print(f"{nx}x{ny}: {ctas} CTAs = {ctas / 444:.2f} waves  micro {ms[2]:.4f} ms  "
-              f"{ns * 1000:.2f} ps/node")
+        print(f"{nx}x{ny}: micro {ms[2]:.4f} ms  {ns * 1000:.3f} ps/node", flush=True)
         s.close()
 
 
