@@ -298,8 +298,15 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         // give 0.412 / 0.398 / 0.409 / 0.410 / 0.409 / 0.390 / 0.438 / 0.419 ms
         // (partial-wave effects dominate at 256 columns); at C4 (1024^2) 64
         // and 56 give 5.47 and 5.51 ms.
+        // Taller blocks take taller bands (fewer pipeline fills per row; the
+        // many waves hide the tail).  Step times measured with
+        // tools/band_bench.py (two alternating rounds, ms/step):
+        //   C3 512^2:  bands 446/66 1.448, uniform 128 1.425, 192 1.504, 256 1.437
+        //   C4 1024^2: uniform 64 5.72, 160 5.60-5.65, 192 5.64-5.68, 256 5.72
+        //   C5 2048^2: uniform 64 23.41, 192 23.10-23.15, 320 22.90-23.04, 384 22.93-23.15
         const char* ly = getenv("MM2D_LY");
-        ctx->ly32 = ly ? std::max(1, atoi(ly)) : 64;
+        const int ly_def = g.by >= 2048 ? 320 : g.by >= 1024 ? 160 : g.by >= 512 ? 128 : 64;
+        ctx->ly32 = ly ? std::max(1, atoi(ly)) : ly_def;
         // explicit band heights (same for every column), e.g. MM2D_BANDS=114,114,22,6
         if (const char* bs = getenv("MM2D_BANDS")) {
             std::vector<int> h;
@@ -317,7 +324,7 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
                 if (acc == g.by) break;
             }
             if (ctx->bands32.back() != g.by) ctx->bands32.clear();   // must cover the block
-        } else if (!ly) {
+        } else if (!ly && g.by < 512) {
             ctx->bands32 = pick_bands(g.bx, g.by, (long long)std::max(occ, 1) * std::max(nsm, 1),
                                       ctx->ly32);
         }
