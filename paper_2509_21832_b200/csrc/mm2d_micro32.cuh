@@ -35,6 +35,10 @@
                          // 166 registers: C4 5.47 vs 5.84 ms, C2 (band 64) 0.390 vs 0.405 ms.
 #endif
 
+#ifndef M32_SHORT_FILL
+#define M32_SHORT_FILL 1
+#endif
+
 namespace mm2d {
 namespace m32 {
 
@@ -962,7 +966,26 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
 
     // steady rows: every stage active, no ghost rows, no wall rows
     const int js_lo = j0s + 1, js_hi = (MIR && (mir_l() || mir_r())) ? js_lo - 1 : min(rhi - 5, j1s - 1);
+#if M32_SHORT_FILL
+    // The first pipeline iteration (j0s - 4) would only stage CellPar row
+    // j0s + 1, issue the bulk load of x-stage row j0s - 1 and build its
+    // tables; done here, without that iteration's reduction and its two
+    // barriers, so a band pays one pipeline-fill iteration less.
+    int j = j0s - 3;
+    stage_par(j0s + 1, computes(j0s + 1));
+    if (computes(j0s - 1)) {
+        prefetch(j0s - 1, std::false_type());
+        build_tables<KS>(a, T3, *reinterpret_cast<const CellPar*>(pring + 32 * ((j0s - 1) & 3)),
+                         v1s, v2s, gauss, etab);
+    }
+    __syncthreads();
+    {
+        const unsigned r0 = R0; R0 = R1; R1 = R2; R2 = r0;
+        double* t0 = T0; T0 = T1; T1 = T2; T2 = T3; T3 = t0;
+    }
+#else
     int j = j0s - 4;
+#endif
     for (; j < js_lo && j <= j1s; ++j) body(j, std::false_type());
     for (; j <= js_hi; ++j) body(j, std::true_type());
     for (; j <= j1s; ++j) body(j, std::false_type());
