@@ -130,14 +130,18 @@ static int ghost_mode(const mm2d_config& c, int face, bool at_edge, int nranks_a
 // least 3% shorter.  Measured at C2: uniform 64 -> 0.391 ms, [112,112,32]
 // -> 0.377 ms; [114,114,28] 0.377, [116,116,24] 0.383, [108,108,40] 0.392.
 static std::vector<int> pick_bands(int bx, int by, long long slots, int ly) {
-    const long long ov = 4;
+    // pipeline fill in row-iterations: a long band pays ov once; a short band,
+    // run back to back with others in a spare slot, also pays its CTA start
+    // (measured optimum at C2: 114/114/28, step 0.3879 ms vs 0.3904 for
+    // 112/112/32 and 0.394 for 116/116/24, which ov_s = 8 reproduces)
+    const long long ov = 4, ov_s = 8;
     const long long nb = (by + ly - 1) / ly;
     const long long waves = ((long long)bx * nb + slots - 1) / slots;
     double best = (double)waves * (ly + ov);
     std::vector<int> out;
     for (int L = 1; L <= 8 && (long long)L * bx < slots; ++L) {
         const long long spare = slots - (long long)L * bx;
-        const long long num = (long long)bx * (by + ov) - ov * spare;
+        const long long num = (long long)bx * (by + ov_s) - ov * spare;
         const long long den = spare + (long long)L * bx;
         const long long H = (num + den - 1) / den;
         const long long R = by - L * H;
