@@ -45,9 +45,7 @@ struct mm2d_ctx {
     double* d_wallg = nullptr;     // wall-strip targets (fast kernel)
     double* d_zero = nullptr;      // V zeros
     bool use32 = false;            // specialised 32 x 32 micro kernel
-    int grid32 = 1;                // persistent CTAs of k_micro32
     std::vector<int> bands32;      // non-uniform band boundaries (empty: uniform ly32)
-    int np32 = 4;                  // node pairs per thread of k_micro32
     int ly32 = 32;
     // context-owned state
     double* d_Qs[2] = {nullptr, nullptr};
@@ -288,7 +286,6 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
         }
     }
     if (ctx->use32) {
-        ctx->np32 = 4;
         int occ = 0, nsm = 0;
         if (m32::setup(&occ) != cudaSuccess) {
             int r = fail_cfg(ctx, "shared memory request too large for k_micro32");
@@ -343,11 +340,6 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
                 fprintf(stderr, "\n");
             }
         }
-        const long long items = (long long)((g.by + ctx->ly32 - 1) / ctx->ly32) * g.bx;
-        const char* pe = getenv("MM2D_PERSIST");
-        const bool persist = pe ? atoi(pe) != 0 : false;
-        const long long slots = (long long)std::max(occ, 1) * std::max(nsm, 1);
-        ctx->grid32 = (int)std::max(1LL, persist ? std::min(slots, items) : items);
     }
     if (cudaFuncSetAttribute(ctx->micro_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)ctx->smem) != cudaSuccess) {
