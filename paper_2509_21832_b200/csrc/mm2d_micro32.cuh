@@ -503,7 +503,6 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     constexpr int KS = 32 / NP_;         // k step between a thread's node pairs
     extern __shared__ __align__(16) double smem[];
     const Geometry& g = a.g;
-    if (*a.err != kNoError) return;
     if (a.part != 0) {
         const int b0 = a.nband ? a.band_j0[blockIdx.y] : blockIdx.y * a.ly;
         const int b1 = a.nband ? a.band_j0[blockIdx.y + 1] : min(g.by, b0 + a.ly);
@@ -524,33 +523,6 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     double* v1s = pring + 4 * 32;
     double* v2s = v1s + NV;
     double* etab = v2s + NV + 2;                    // [64] 2^(i/64)
-    if (tid < NV) v1s[tid] = a.v1[tid];
-    else if (tid < 2 * NV) v2s[tid - NV] = a.v2[tid - NV];
-    if (tid < 64) etab[tid] = kExp2Tab[tid];
-
-    const bool gauss = a.gauss && !(a.eps < 1e-10 &&
-        __longlong_as_double(a.iso[0]) <= 1e-13 * __longlong_as_double(a.iso[3]) &&
-        __longlong_as_double(a.iso[1]) <= 1e-13 * __longlong_as_double(a.iso[3]) &&
-        __longlong_as_double(a.iso[2]) <= 1e-13 * __longlong_as_double(a.iso[3]));
-    __syncthreads();
-
-    // per-thread constants: node offsets and sign-folded upwind coefficients
-    // Y = c (G_self - G_upwind): the reference's v (G_i - G_{i-1}) / d for
-    // v >= 0 and v (G_{i+1} - G_i) / d for v < 0 (_core.pyx:152-168)
-    // node-pair offsets: off(p) = off0 + 256 p into a cell's block,
-    // koff(p) = koff0 + 64 p into the K-table (immediate offsets in SASS)
-    const int off0 = 32 * kb + lb;
-    const int koff0 = KT + KW * kb;
-#define off_(p) (off0 + 32 * KS * (p))
-#define koff_(p) (koff0 + KW * KS * (p))
-    double cx[NP_];
-#pragma unroll
-    for (int p = 0; p < NP_; ++p)
-        cx[p] = (p < NP_ / 2 ? -a.dt : a.dt) * v1s[kb + KS * p] * a.idx;
-    const bool negy = v2s[lb] < 0.0;
-    const double sy = negy ? -a.dt : a.dt;
-    const double cy0 = sy * v2s[lb] * a.idy, cy1 = sy * v2s[lb + 1] * a.idy;
-    const int xsel = lp * 4;       // this thread's cross-term table row
     const size_t V_ = V;
 
     const int i = blockIdx.x;
@@ -605,11 +577,11 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                        reinterpret_cast<const double*>(a.P + ring_index(g, i, r)) + 2 * tid);
         cp_async_commit();
     };
+    // Every CTA start waits on memory several times (its first CellPar rows,
+    // its first bulk G row, the error word, the velocity axes): issue the
+    // asynchronous copies first so those latencies overlap.
     stage_par(j0s - 1, computes(j0s - 1));
     stage_par(j0s, computes(j0s));
-    cp_async_wait_all();
-    __syncthreads();
-
     // x-stage rows arrive by TMA: own row -> stg[0:V], the right neighbour's
     // k < 16 half -> stg[V:V+V/2], the left neighbour's k >= 16 half ->
     // stg[V+V/2:2V], so every node's upwind neighbour sits at the node's own
@@ -620,20 +592,6 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         mbar_init(mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    // the G* ring: 64 TMEM columns, allocated by warp 0
-    unsigned* tslot = reinterpret_cast<unsigned*>(etab + 64);
-    if (tid < 32) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                         smem_u32(tslot)),
-                     "n"(TM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const unsigned tbase = *reinterpret_cast<volatile unsigned*>(tslot);
-    const unsigned tq = tbase + ((unsigned)(tid & ~31) << 16);   // this warp's lane quadrant
     unsigned nload = 0;            // bulk loads issued (mbarrier phase = parity)
     auto prefetch = [&](int r, auto steady) {
         if (tid != 0) { ++nload; return; }
@@ -658,6 +616,59 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         ++nload;
     };
 
+    if (computes(j0s - 1)) prefetch(j0s - 1, std::false_type());
+    if (*a.err != kNoError) {
+        // an earlier stage failed: leave the step's inputs untouched, after
+        // the copies in flight have landed
+        cp_async_wait_all();
+        if (tid == 0 && nload) mbar_wait(mbar, 0);
+        __syncthreads();
+        return;
+    }
+    if (tid < NV) v1s[tid] = a.v1[tid];
+    else if (tid < 2 * NV) v2s[tid - NV] = a.v2[tid - NV];
+    if (tid < 64) etab[tid] = kExp2Tab[tid];
+
+    const bool gauss = a.gauss && !(a.eps < 1e-10 &&
+        __longlong_as_double(a.iso[0]) <= 1e-13 * __longlong_as_double(a.iso[3]) &&
+        __longlong_as_double(a.iso[1]) <= 1e-13 * __longlong_as_double(a.iso[3]) &&
+        __longlong_as_double(a.iso[2]) <= 1e-13 * __longlong_as_double(a.iso[3]));
+    __syncthreads();
+
+    // per-thread constants: node offsets and sign-folded upwind coefficients
+    // Y = c (G_self - G_upwind): the reference's v (G_i - G_{i-1}) / d for
+    // v >= 0 and v (G_{i+1} - G_i) / d for v < 0 (_core.pyx:152-168)
+    // node-pair offsets: off(p) = off0 + 256 p into a cell's block,
+    // koff(p) = koff0 + 64 p into the K-table (immediate offsets in SASS)
+    const int off0 = 32 * kb + lb;
+    const int koff0 = KT + KW * kb;
+#define off_(p) (off0 + 32 * KS * (p))
+#define koff_(p) (koff0 + KW * KS * (p))
+    double cx[NP_];
+#pragma unroll
+    for (int p = 0; p < NP_; ++p)
+        cx[p] = (p < NP_ / 2 ? -a.dt : a.dt) * v1s[kb + KS * p] * a.idx;
+    const bool negy = v2s[lb] < 0.0;
+    const double sy = negy ? -a.dt : a.dt;
+    const double cy0 = sy * v2s[lb] * a.idy, cy1 = sy * v2s[lb + 1] * a.idy;
+    const int xsel = lp * 4;       // this thread's cross-term table row
+    cp_async_wait_all();
+    __syncthreads();
+
+    // the G* ring: 64 TMEM columns, allocated by warp 0
+    unsigned* tslot = reinterpret_cast<unsigned*>(etab + 64);
+    if (tid < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(tslot)),
+                     "n"(TM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const unsigned tbase = *reinterpret_cast<volatile unsigned*>(tslot);
+    const unsigned tq = tbase + ((unsigned)(tid & ~31) << 16);   // this warp's lane quadrant
     // rotating slot pointers: ring rows (j-1, j, j+1); table rows
     // (j, j+1, j+2, j+3, j-1)
     unsigned R0 = tq, R1 = tq + 16, R2 = tq + 32;   // TMEM ring rows (j-1, j, j+1)
@@ -968,13 +979,12 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     const int js_lo = j0s + 1, js_hi = (MIR && (mir_l() || mir_r())) ? js_lo - 1 : min(rhi - 5, j1s - 1);
 #if M32_SHORT_FILL
     // The first pipeline iteration (j0s - 4) would only stage CellPar row
-    // j0s + 1, issue the bulk load of x-stage row j0s - 1 and build its
-    // tables; done here, without that iteration's reduction and its two
+    // j0s + 1, issue the bulk load of x-stage row j0s - 1 (issued at entry)
+    // and build its tables; done here, without that iteration's reduction and its two
     // barriers, so a band pays one pipeline-fill iteration less.
     int j = j0s - 3;
     stage_par(j0s + 1, computes(j0s + 1));
-    if (computes(j0s - 1)) {
-        prefetch(j0s - 1, std::false_type());
+    if (computes(j0s - 1)) {   // (its bulk load was issued at entry)
         build_tables<KS>(a, T3, *reinterpret_cast<const CellPar*>(pring + 32 * ((j0s - 1) & 3)),
                          v1s, v2s, gauss, etab);
     }
