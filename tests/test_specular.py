@@ -215,6 +215,26 @@ def test_gpu_specular_block_grid_equals_serial_bitwise(mm, grid, nv):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("nv", [6, 32])
+def test_gpu_specular_overlap_split_equals_serial(mm, nv):
+    """Blocks large enough that the split micro launch has interior CTAs
+    (run while the G halo is in flight) and perimeter CTAs, with specular
+    faces on the physical boundary: still bitwise the serial step."""
+    from paper_2509_21832_b200.parallel import run_parallel_2d
+    S = mm.SPECULAR
+    nx, ny = 24, 400
+    mesh, bc, model = _problem(nx, ny, (S, S, S, S), nv=nv, vmax=5.0)
+    Q0, G0 = _state(nx, ny, nv, seed=12, amp=1e-2)
+    dt = 0.3 * (1.0 / ny) / 5.0
+    Qp, Gp, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, 3, grid=(2, 2))
+    st = mm.State2D(0.0, Q0, G0)
+    for _ in range(3):
+        st = mm.step_2d(st, mesh, bc, 0.08, model, dt)
+    assert np.array_equal(Qp, st.Q)
+    assert np.array_equal(Gp, st.G)
+
+
+@pytest.mark.gpu
 def test_gpu_specular_needs_symmetric_velocity_axis(mm):
     mesh = mm.PhaseMesh(space=(mm.Axis(0, 1, 4), mm.Axis(0, 1, 4)),
                         velocity=(mm.Axis(-6.0, 7.0, 12), mm.Axis(-7.0, 7.0, 12)))
