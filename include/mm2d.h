@@ -118,7 +118,9 @@ int mm2d_step(mm2d_ctx *ctx, const double *d_Q, const double *d_G, double dt,
  * be split around the G halo exchange so the exchange overlaps interior-cell
  * compute: phase 2 = prep + the micro CTAs that read no received G halo
  * (needs only the Q halo), phase 3 = the remaining micro CTAs (after the G
- * halo has landed); 2 then 3 is bitwise identical to 0. */
+ * halo has landed); 2 then 3 is bitwise identical to 0.  Finer still,
+ * phase 4 = prep only and phase 5 = the interior micro CTAs only, so 3 can
+ * run on a second stream concurrently with 5 (4, 5 | 3 is bitwise 0). */
 int mm2d_step_phase(mm2d_ctx *ctx, int phase, const double *d_Q, const double *d_G, double dt,
                     double *d_Qout, double *d_Gout, double *d_H,
                     int nsrc, const double *d_src_coeffs, const double *d_src_shapes,

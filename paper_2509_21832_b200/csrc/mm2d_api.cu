@@ -446,7 +446,9 @@ static int grid_for(long long n, int threads) {
 static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double dt, double* Qout,
                         double* Gout, double* H, int nsrc, const double* sc, const double* ss,
                         const double* qsrc, cudaStream_t s, cudaEvent_t* ev = nullptr,
-                        int phases = 3, int part = 0) {
+                        int phases = 3, int part = 0, int mode = 0) {
+    // part: micro CTAs launched (0 all, 1 those that read no received G halo,
+    // 2 the others); mode: 0 prep + micro, 1 prep only, 2 micro only
 #define MARK(q) \
     if (ev) CK(cudaEventRecord(ev[q], s))
     const Geometry& g = ctx->g;
@@ -455,7 +457,9 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     const bool gauss = c.nu != 0.0;
     // isotropy maxima for the eps < 1e-10 guard (micro2d.py:96)
     long long nl = 0;
-    if (gauss && c.eps < 1e-10) {
+    if (gauss && c.eps < 1e-10 && (phases & 1) && mode != 2) {
+        // (reset by the call that runs k_prep, which rebuilds the maxima; a
+        // micro-only call of a split step reads them)
         CK(cudaMemsetAsync(ctx->d_err + 1, 0, sizeof(unsigned long long) * 4, s));
     }
     ctx->last_dt = dt;
@@ -476,7 +480,7 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     pa.step = 0;
     pa.gauss = gauss;
     pa.h2x = 0.5 / g.dx; pa.h2y = 0.5 / g.dy;
-    if (part != 2) {   // the halo part of a split micro launch reuses the prep of part 1
+    if (mode != 2) {
         k_prep<<<grid_for(ring, 128), 128, 0, s>>>(pa);
         ++nl;
     }
@@ -495,8 +499,13 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     ma.wall_ghat = ctx->d_wallg;
     ma.zero = ctx->d_zero;
     ma.part = part;
-    if (ctx->use32 && nsrc == 0) {
-        if (ctx->d_wallg && part != 2) {
+    if (mode == 1) {
+        if (ctx->use32 && nsrc == 0 && ctx->d_wallg) {
+            m32::launch_wall_ghat(ma, ctx->d_wallg, 2 * g.by + 2 * g.bx, s);
+            ++nl;
+        }
+    } else if (ctx->use32 && nsrc == 0) {
+        if (ctx->d_wallg && mode != 2) {
             m32::launch_wall_ghat(ma, ctx->d_wallg, 2 * g.by + 2 * g.bx, s);
             ++nl;
         }
@@ -514,7 +523,7 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
         CK(cudaLaunchKernel(ctx->micro_fn, grid, dim3(ctx->NT), args, ctx->smem, s));
     }
     MARK(3);
-    nl += 1;
+    if (mode != 1) nl += 1;
     }   // phase 0: prep (with the Q ring), micro
     if (phases & 2) {
     MARK(4);   // (heat ghosts are resolved inside the sweeps)
@@ -546,13 +555,17 @@ extern "C" int mm2d_step_phase(mm2d_ctx* ctx, int phase, const double* d_Q, cons
                                double dt, double* d_Qout, double* d_Gout, double* d_H, int nsrc,
                                const double* d_src_coeffs, const double* d_src_shapes,
                                const double* d_qsrc, void* stream) {
-    if (!ctx || phase < 0 || phase > 3) return fail_cfg(ctx, "phase must be 0, 1, 2 or 3");
+    if (!ctx || phase < 0 || phase > 5) return fail_cfg(ctx, "phase must be 0 to 5");
     CK(cudaSetDevice(ctx->dev));
-    // 2 / 3: phase 0 split around the G halo exchange -- prep and the micro
-    // CTAs that read no received halo, then the CTAs that do
+    // phase 0 split around the G halo exchange: 2 = prep + the micro CTAs
+    // that read no received halo, 3 = the CTAs that do; or finer, so the two
+    // micro parts can run concurrently on two streams: 4 = prep only, 5 = the
+    // interior micro CTAs only
+    static const int part_of[6] = {0, 0, 1, 2, 0, 1};
+    static const int mode_of[6] = {0, 0, 0, 2, 1, 2};
     return enqueue_step(ctx, d_Q, d_G, dt, d_Qout, d_Gout, d_H, nsrc, d_src_coeffs,
                         d_src_shapes, d_qsrc, (cudaStream_t)stream, nullptr,
-                        phase == 1 ? 2 : 1, phase >= 2 ? phase - 1 : 0);
+                        phase == 1 ? 2 : 1, part_of[phase], mode_of[phase]);
 }
 
 extern "C" int mm2d_step(mm2d_ctx* ctx, const double* d_Q, const double* d_G, double dt,

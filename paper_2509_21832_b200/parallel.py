@@ -258,6 +258,11 @@ class BlockStepper:
         self.plan = plan
         self.solver = Solver2D(mesh, bc, eps, model, grid=grid, rank=plan.pos, device=device)
         self.bufs = halo_buffers(self.solver)
+        import torch
+        with torch.cuda.device(device):
+            self.side = torch.cuda.Stream(device)   # the perimeter micro CTAs of a split step
+            self.ev_prep = torch.cuda.Event()
+            self.ev_side = torch.cuda.Event()
 
     def _stream(self):
         import torch
@@ -288,9 +293,11 @@ def step_blocks(blocks, exchange, states, dt):
     The G ring exchange (V doubles per perimeter cell, the bulk of the
     traffic) overlaps the interior cells' micro update: the Q ring (6
     doubles per cell) is exchanged first, then the G exchange is posted, the
-    prep and every micro CTA that reads no received G halo run (phase 2),
-    and only the perimeter CTAs (phase 3) wait for the G halo.  Phases 2 + 3
-    are bitwise the unsplit phase 0."""
+    prep (phase 4) and every micro CTA that reads no received G halo (phase
+    5) are enqueued, and only the perimeter CTAs (phase 3) wait for the G
+    halo -- on a side stream that waits for the prep and the exchange, so
+    they run concurrently with the interior CTAs instead of after them.
+    Phases 4 + 5 + 3 are bitwise the unsplit phase 0."""
     import torch
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
@@ -303,12 +310,23 @@ def step_blocks(blocks, exchange, states, dt):
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
             b.unpack(FIELD_Q)
-            b.phase(2, st[0], st[1], dt, st[2], st[3], st[4])
-    exchange.finish(hg)
+            b.phase(4, st[0], st[1], dt, st[2], st[3], st[4])
+            b.ev_prep.record()
+            b.phase(5, st[0], st[1], dt, st[2], st[3], st[4])
+    # the perimeter CTAs on each block's side stream, after its prep and the
+    # G exchange (a stream-side wait over NCCL)
+    for b in blocks:
+        with torch.cuda.device(b.solver.device), torch.cuda.stream(b.side):
+            b.side.wait_event(b.ev_prep)
+    with torch.cuda.device(blocks[0].solver.device), torch.cuda.stream(blocks[0].side):
+        exchange.finish(hg)
     _sync_devices(blocks)
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
-            b.phase(3, st[0], st[1], dt, st[2], st[3], st[4])
+            with torch.cuda.stream(b.side):
+                b.phase(3, st[0], st[1], dt, st[2], st[3], st[4])
+                b.ev_side.record()
+            torch.cuda.current_stream().wait_event(b.ev_side)
             b.pack(FIELD_H, None)
     _sync_devices(blocks)
     exchange.exchange(FIELD_H)

@@ -169,8 +169,9 @@ def test_opposite_slots_are_involutions():
 def test_step_blocks_overlaps_g_exchange_with_interior_micro(monkeypatch):
     """step_blocks' order of operations (host logic, no GPU): the Q ring is
     exchanged first, the G exchange is posted and left in flight while the
-    prep + interior micro CTAs (phase 2) are enqueued, the perimeter CTAs
-    (phase 3) only after it completes, then the heat ring and the macro
+    prep (phase 4) and the interior micro CTAs (phase 5) are enqueued, the
+    perimeter CTAs (phase 3) go on the side stream after the prep and the G
+    exchange, the main stream joins them, then the heat ring and the macro
     phase -- the reference worker grid's two barrier points
     (parallel.py:384-394) with the G transfer hidden behind interior work."""
     import contextlib
@@ -179,7 +180,36 @@ def test_step_blocks_overlaps_g_exchange_with_interior_micro(monkeypatch):
     log = []
     monkeypatch.setattr(torch.cuda, "device", lambda d: contextlib.nullcontext())
 
+    class Stream:
+        def __init__(self, name):
+            self.name = name
+
+        def wait_event(self, ev):
+            log.append(("wait", self.name, ev.name))
+
+    class Event:
+        def __init__(self, name):
+            self.name = name
+
+        def record(self):
+            log.append(("record", self.name))
+
+    cur = [Stream("main")]
+
+    @contextlib.contextmanager
+    def stream_ctx(st):
+        prev, cur[0] = cur[0], st
+        yield
+        cur[0] = prev
+
+    monkeypatch.setattr(torch.cuda, "stream", stream_ctx)
+    monkeypatch.setattr(torch.cuda, "current_stream", lambda *a: cur[0])
+
     class Blk:
+        side = Stream("side")
+        ev_prep = Event("prep")
+        ev_side = Event("side")
+
         class solver:
             device = torch.device("cpu")
 
@@ -190,7 +220,7 @@ def test_step_blocks_overlaps_g_exchange_with_interior_micro(monkeypatch):
             log.append(("unpack", f))
 
         def phase(self, ph, *args):
-            log.append(("phase", ph))
+            log.append(("phase", ph, cur[0].name))
 
     class Ex:
         def exchange(self, f):
@@ -201,10 +231,12 @@ def test_step_blocks_overlaps_g_exchange_with_interior_micro(monkeypatch):
             return f
 
         def finish(self, h):
-            log.append(("finish", h))
+            log.append(("finish", h, cur[0].name))
 
     par.step_blocks([Blk()], Ex(), [(None,) * 5], 1e-3)
     G, Q, H = par.FIELD_G, par.FIELD_Q, par.FIELD_H
     assert log == [("pack", Q), ("pack", G), ("exchange", Q), ("start", G), ("unpack", Q),
-                   ("phase", 2), ("finish", G), ("phase", 3), ("pack", H), ("exchange", H),
-                   ("unpack", H), ("phase", 1)]
+                   ("phase", 4, "main"), ("record", "prep"), ("phase", 5, "main"),
+                   ("wait", "side", "prep"), ("finish", G, "side"), ("phase", 3, "side"),
+                   ("record", "side"), ("wait", "main", "side"), ("pack", H),
+                   ("exchange", H), ("unpack", H), ("phase", 1, "main")]
