@@ -35,6 +35,9 @@
                          // 166 registers: C4 5.47 vs 5.84 ms, C2 (band 64) 0.390 vs 0.405 ms.
 #endif
 
+#ifndef M32_NS
+#define M32_NS 8   // reducer threads per reduced value (the shuffle levels are log2 of it)
+#endif
 #ifndef M32_SHORT_FILL
 #define M32_SHORT_FILL 1
 #endif
@@ -209,7 +212,7 @@ __device__ __forceinline__ void reduce12_begin(const double (&v)[12], double* sr
 
 template <int NT_>
 __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
-    constexpr int NS = NT_ >= 128 ? 8 : 4;  // segments per value (threads per value)
+    constexpr int NS = NT_ >= 128 ? M32_NS : 4;  // segments per value (threads per value)
     constexpr int SEG = NT_ / NS;           // partials per (value, segment)
     constexpr int L2N = SEG / 2;            // double2 loads per segment
     // the reducers are the LAST 12 * NS threads (warps 1-3 at NT = 128), so
@@ -233,9 +236,9 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
 #pragma unroll
             for (int q = 0; q < L2N; q += 2 * w) u[q] += u[q + w];
         double acc = u[0];
-        if (NS == 8) acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (NS >= 8) acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        if (NS >= 4) acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (NS >= 2) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
         if (act && seg == 0) sred[12 * NT_ + vid] = acc;
     }
     __syncthreads();
