@@ -51,12 +51,17 @@ constexpr int NT = 128;              // threads of the default 8-node (NP = 4) v
 constexpr int NP = 4;                // node pairs per thread (default variant)
 constexpr int TSLOTS = 4;            // table slots (rows j..j+3; the slot rebuilt
                                      // at iteration j last held row j-1)
+#ifndef M32_W1POW_TABLE
 #if MICRO32_MINB >= 4
 #define M32_W1POW_TABLE 0            // 4 CTAs/SM: recompute W1^2, W1^3 to fit 56 KB
-constexpr int KW = 10;               // K-table entries per k
 #else
 #define M32_W1POW_TABLE 1
+#endif
+#endif
+#if M32_W1POW_TABLE
 constexpr int KW = 12;               // K-table entries per k
+#else
+constexpr int KW = 10;               // K-table entries per k
 #endif
 constexpr int KT = 0;                // K-table [32][KW]
 constexpr int LT = KT + KW * NV;     // L-table [8][32]
