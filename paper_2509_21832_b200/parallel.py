@@ -318,8 +318,7 @@ def step_blocks(blocks, exchange, states, dt):
     for b in blocks:
         with torch.cuda.device(b.solver.device), torch.cuda.stream(b.side):
             b.side.wait_event(b.ev_prep)
-    with torch.cuda.device(blocks[0].solver.device), torch.cuda.stream(blocks[0].side):
-        exchange.finish(hg)
+            exchange.finish(hg)   # (a started exchange may be finished more than once)
     _sync_devices(blocks)
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
