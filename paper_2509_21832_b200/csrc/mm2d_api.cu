@@ -13,6 +13,12 @@
 #include <vector>
 
 #include "mm2d.h"
+
+// k_prep_tiled (shared-memory neighbour primitives) or the one-thread-per-
+// cell k_prep; both produce the same CellPar bits
+#ifndef MM2D_PREP_TILED
+#define MM2D_PREP_TILED 1
+#endif
 #include "mm2d_common.cuh"
 #include "mm2d_contract.cuh"
 #include "mm2d_macro.cuh"
@@ -481,7 +487,22 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     pa.gauss = gauss;
     pa.h2x = 0.5 / g.dx; pa.h2y = 0.5 / g.dy;
     if (mode != 2) {
+#if MM2D_PREP_TILED
+        {
+            const int nt = ((g.bx + 2 + PT_I - 1) / PT_I) * ((g.by + 2 + PT_J - 1) / PT_J);
+            static std::atomic<bool> attr[64];   // per device: the attribute is per context
+            int dev = 0;
+            CK(cudaGetDevice(&dev));
+            if (dev < 0 || dev >= 64 || !attr[dev].load()) {
+                CK(cudaFuncSetAttribute(k_prep_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kPrepStageBytes));
+                if (dev >= 0 && dev < 64) attr[dev] = true;
+            }
+            k_prep_tiled<<<std::max(1, std::min(nt, 148 * 8)), PT_THREADS, kPrepStageBytes, s>>>(pa);
+        }
+#else
         k_prep<<<grid_for(ring, 128), 128, 0, s>>>(pa);
+#endif
         ++nl;
     }
     MARK(2);

@@ -210,12 +210,15 @@ __device__ __forceinline__ void prims_fast(const double* q, double& rho, double&
 // the modified tensor with its SPD check (gas_state.py:138-146), the
 // isotropy maxima (micro2d.py:63-67) and the diffuse-wall ghost densities
 // of edge cells (boundary.py:248-290).
-__global__ void k_prep(PrepArgs a) {
+//
+// NB holds the neighbour primitives of an owned cell: nb(s, d, k) is
+// component k (u1, u2, T) of the neighbour at offset s ? +1 : -1 along axis d
+// (0 x, 1 y), as prims_fast gives them.
+template <class NB, class ST>
+__device__ __forceinline__ void prep_cell(const PrepArgs& a, int t, int i, int j, const NB& nb,
+                                          const ST& store) {
     const Geometry& g = a.g;
-    if (*a.err != kNoError) return;
-    const int n = (g.bx + 2) * (g.by + 2);
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
+    {
         const bool own = i >= 0 && i < g.bx && j >= 0 && j < g.by;
         // the ring fill (extract_ring rules) fused in: this cell's state from
         // Q / a received halo cell, written to the ring for the macro sweeps
@@ -284,16 +287,10 @@ __global__ void k_prep(PrepArgs a) {
         if (own) {
             // centred differences over the ring (extend_macro_scalar_2d:
             // wrap for periodic, copy otherwise)
-            double r_, xu1[2], xu2[2], xT[2], yu1[2], yu2[2], yT[2];
-            double a11, a12, a22;
+            double xu1[2], xu2[2], xT[2], yu1[2], yu2[2], yT[2];
             for (int s = 0; s < 2; ++s) {
-                double qn[6];
-                load_ring_q(g, a.Q, a.Qr, i + (s ? 1 : -1), j, qn);
-                prims_fast(qn, r_, xu1[s], xu2[s], a11, a12, a22);
-                xT[s] = 0.5 * (a11 + a22);
-                load_ring_q(g, a.Q, a.Qr, i, j + (s ? 1 : -1), qn);
-                prims_fast(qn, r_, yu1[s], yu2[s], a11, a12, a22);
-                yT[s] = 0.5 * (a11 + a22);
+                xu1[s] = nb(s, 0, 0); xu2[s] = nb(s, 0, 1); xT[s] = nb(s, 0, 2);
+                yu1[s] = nb(s, 1, 0); yu2[s] = nb(s, 1, 1); yT[s] = nb(s, 1, 2);
             }
             const double du1x = (xu1[1] - xu1[0]) * a.h2x;
             const double du2x = (xu2[1] - xu2[0]) * a.h2x;
@@ -309,7 +306,98 @@ __global__ void k_prep(PrepArgs a) {
             if (g.wall[2] && j == 0) P.rw[2] = wall_density(rho, u2, t22, g.wallT[2], -1.0);
             if (g.wall[3] && j == g.by - 1) P.rw[3] = wall_density(rho, u2, t22, g.wallT[3], 1.0);
         }
-        reinterpret_cast<CellPar*>(a.P)[t] = P;
+        store(P);
+    }
+}
+
+// (u1, u2, T) of ring cell (i, j) as the centred gradients use them
+__device__ __forceinline__ void nb_prims(const PrepArgs& a, int i, int j, double* w) {
+    double qn[6], r_, a11, a12, a22;
+    load_ring_q(a.g, a.Q, a.Qr, i, j, qn);
+    prims_fast(qn, r_, w[0], w[1], a11, a12, a22);
+    w[2] = 0.5 * (a11 + a22);
+}
+
+// One thread per ring cell; each owned cell re-derives its four neighbours'
+// primitives from Q (the reference's extend + centred difference).
+__global__ void k_prep(PrepArgs a) {
+    const Geometry& g = a.g;
+    if (*a.err != kNoError) return;
+    const int n = (g.bx + 2) * (g.by + 2);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
+        double w[2][2][3];
+        if (i >= 0 && i < g.bx && j >= 0 && j < g.by) {
+            for (int s = 0; s < 2; ++s) {
+                nb_prims(a, i + (s ? 1 : -1), j, w[s][0]);
+                nb_prims(a, i, j + (s ? 1 : -1), w[s][1]);
+            }
+        }
+        prep_cell(a, t, i, j, [&](int s, int d, int k) { return w[s][d][k]; },
+                  [&](const CellPar& P) { reinterpret_cast<CellPar*>(a.P)[t] = P; });
+    }
+}
+
+// Tiled variant: a CTA owns a PT_I x PT_J tile of ring cells.  It first
+// derives (u1, u2, T) once per cell of the tile plus its one-cell halo into
+// shared memory, then every cell of the tile reads its neighbours from
+// there: one Q load and one primitive evaluation per cell instead of five,
+// and the same prims_fast arithmetic, so the CellPar bits are unchanged.
+constexpr int PT_I = 8, PT_J = 32, PT_THREADS = PT_I * PT_J;
+constexpr size_t kPrepStageBytes = sizeof(CellPar) * PT_THREADS;
+
+__device__ __forceinline__ int prep_tiles(const Geometry& g) {
+    return ((g.bx + 2 + PT_I - 1) / PT_I) * ((g.by + 2 + PT_J - 1) / PT_J);
+}
+
+__global__ void __launch_bounds__(PT_THREADS) k_prep_tiled(PrepArgs a) {
+    const Geometry& g = a.g;
+    if (*a.err != kNoError) return;
+    __shared__ double sw[3][PT_I + 2][PT_J + 2];
+    extern __shared__ double stage[];   // [PT_THREADS][32] CellPar staging (swizzled)
+    const int ntj = (g.by + 2 + PT_J - 1) / PT_J;
+    const int ntiles = prep_tiles(g);
+    const int li = threadIdx.x / PT_J, lj = threadIdx.x % PT_J;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int ri0 = (tile / ntj) * PT_I, rj0 = (tile % ntj) * PT_J;
+        __syncthreads();   // the previous tile's readers are done
+        // halo cell (hi, hj) is cell (ri0 + hi - 2, rj0 + hj - 2); only the
+        // neighbours of owned cells, i in [-1, bx] and j in [-1, by], are used
+        for (int h = threadIdx.x; h < (PT_I + 2) * (PT_J + 2); h += PT_THREADS) {
+            const int hi = h / (PT_J + 2), hj = h % (PT_J + 2);
+            const int i = ri0 + hi - 2, j = rj0 + hj - 2;
+            if (i < -1 || i > g.bx || j < -1 || j > g.by) continue;
+            double w[3];
+            nb_prims(a, i, j, w);
+            sw[0][hi][hj] = w[0]; sw[1][hi][hj] = w[1]; sw[2][hi][hj] = w[2];
+        }
+        __syncthreads();
+        const int ri = ri0 + li, rj = rj0 + lj;
+        const int nrow = min(PT_J, g.by + 2 - rj0);   // cells of this tile row
+        double* st = stage + threadIdx.x * 32;
+        if (ri < g.bx + 2 && rj < g.by + 2) {
+            prep_cell(a, ri * (g.by + 2) + rj, ri - 1, rj - 1, [&](int s, int d, int k) {
+                const int di = d == 0 ? (s ? 2 : 0) : 1, dj = d == 1 ? (s ? 2 : 0) : 1;
+                return sw[k][li + di][lj + dj];
+            }, [&](const CellPar& P) {
+                // stage with an XOR swizzle (bank = e ^ lane: conflict-free)
+                const double* pv = reinterpret_cast<const double*>(&P);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) st[e ^ lj] = pv[e];
+            });
+        }
+        __syncwarp();
+        // the warp's tile row is nrow contiguous CellPars: write them as
+        // 512-byte coalesced runs of double2
+        if (ri < g.bx + 2) {
+            double* dst = reinterpret_cast<double*>(a.P) + ((size_t)ri * (g.by + 2) + rj0) * 32;
+            const double* wst = stage + (threadIdx.x - lj) * 32;
+            for (int f = 2 * lj; f < nrow * 32; f += 64) {
+                const int c = f >> 5, e = f & 31;
+                const double x0 = wst[c * 32 + (e ^ c)], x1 = wst[c * 32 + ((e + 1) ^ c)];
+                *reinterpret_cast<double2*>(dst + f) = make_double2(x0, x1);
+            }
+        }
     }
 }
 
