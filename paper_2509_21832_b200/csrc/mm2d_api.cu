@@ -498,10 +498,11 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
                                         (int)kPrepStageBytes));
                 if (dev >= 0 && dev < 64) attr[dev] = true;
             }
-            k_prep_tiled<<<std::max(1, std::min(nt, 148 * 8)), PT_THREADS, kPrepStageBytes, s>>>(pa);
+            CK(launch_pdl(k_prep_tiled, dim3(std::max(1, std::min(nt, 148 * 8))), dim3(PT_THREADS),
+                          kPrepStageBytes, s, pa));
         }
 #else
-        k_prep<<<grid_for(ring, 128), 128, 0, s>>>(pa);
+        CK(launch_pdl(k_prep, dim3(grid_for(ring, 128)), dim3(128), 0, s, pa));
 #endif
         ++nl;
     }
@@ -557,10 +558,11 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     {
         const int jlo = g.qylo == GM_HALO ? -1 : 0, jhi = g.qyhi == GM_HALO ? g.by : g.by - 1;
         dim3 gx((g.bx + MX_TI - 1) / MX_TI, (jhi - jlo + 1 + MX_TJ - 1) / MX_TJ);
-        k_macro_x<<<gx, dim3(MX_TJ, MX_TI + 2), 0, s>>>(mc);
+        CK(launch_pdl(k_macro_x, gx, dim3(MX_TJ, MX_TI + 2), 0, s, mc));
     }
     MARK(5);
-    k_macro_y<<<dim3((g.by + MY_OUT - 1) / MY_OUT, (g.bx + 3) / 4), 128, 0, s>>>(mc);
+    CK(launch_pdl(k_macro_y, dim3((g.by + MY_OUT - 1) / MY_OUT, (g.bx + 3) / 4), dim3(128), 0, s,
+                  mc));
     MARK(6);
     nl += 2;
     MARK(7);   // (the SoA heat output is written by k_macro_y)

@@ -14,6 +14,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace mm2d {
 
@@ -83,6 +84,37 @@ struct Geometry {
 
 __host__ __device__ inline int ring_index(const Geometry& g, int i, int j) {
     return (i + 1) * (g.by + 2) + (j + 1);
+}
+
+// Programmatic dependent launch: the step's kernels are launched with
+// programmatic stream serialization (launch_pdl), so a kernel's CTAs can be
+// resident before its predecessor has finished.  Every such kernel waits for
+// the predecessor's completion and memory flush first, then lets its own
+// successor be scheduled.  (Both are no-ops under a normal launch.)
+template <bool kTrigger = true>
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (kTrigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+#ifndef MM2D_PDL
+#define MM2D_PDL 0   // measured slower at C2: off
+#endif
+// launch with programmatic stream serialization (MM2D_PDL=0: a plain launch)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = MM2D_PDL;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, kernel, std::forward<Args>(args)...);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

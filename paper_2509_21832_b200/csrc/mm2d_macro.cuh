@@ -133,6 +133,7 @@ constexpr int MX_TJ = 32;                // cells per CTA along y (one warp row)
 
 // x-sweep: block (32, MX_TI + 2); thread (lane, r) owns cell (i0 - 1 + r, j)
 __global__ void __launch_bounds__(MX_TJ * (MX_TI + 2)) k_macro_x(MacroArgs a) {
+    pdl_enter();
     __shared__ double sL[MX_TI + 2][6][MX_TJ], sR[MX_TI + 2][6][MX_TJ];
     const Geometry& g = a.g;
     if (*a.err != kNoError) return;
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(MX_TJ * (MX_TI + 2)) k_macro_x(MacroArgs a) {
 // j0 - 1 + l and takes its neighbours' half fluxes by shuffles
 constexpr int MY_OUT = 30;
 __global__ void __launch_bounds__(128) k_macro_y(MacroArgs a) {
+    pdl_enter();
     const Geometry& g = a.g;
     if (*a.err != kNoError) return;
     const int lane = threadIdx.x & 31;

@@ -40,12 +40,12 @@ void launch_micro32(const MicroArgs& a, dim3 grid, cudaStream_t s) {
     const Geometry& g = a.g;
     const bool mir = g.xlo == GM_MIRROR || g.xhi == GM_MIRROR || g.ylo == GM_MIRROR ||
                      g.yhi == GM_MIRROR;
-    if (mir) k_micro32<4, true><<<grid, 128, smem_bytes_v3<4>(), s>>>(a);
-    else k_micro32<4, false><<<grid, 128, smem_bytes_v3<4>(), s>>>(a);
+    if (mir) launch_pdl(k_micro32<4, true>, grid, dim3(128), smem_bytes_v3<4>(), s, a);
+    else launch_pdl(k_micro32<4, false>, grid, dim3(128), smem_bytes_v3<4>(), s, a);
 }
 
 void launch_wall_ghat(const MicroArgs& a, double* out, int nblocks, cudaStream_t s) {
-    k_wall_ghat<<<nblocks, 128, 0, s>>>(a, out);
+    launch_pdl(k_wall_ghat, dim3(nblocks), dim3(128), 0, s, a, out);
 }
 
 }  // namespace m32

@@ -38,6 +38,9 @@
 #ifndef M32_NS
 #define M32_NS 8   // reducer threads per reduced value (the shuffle levels are log2 of it)
 #endif
+#ifndef M32_PDL_TRIGGER
+#define M32_PDL_TRIGGER 0
+#endif
 #ifndef M32_SHORT_FILL
 #define M32_SHORT_FILL 1
 #endif
@@ -506,6 +509,9 @@ inline size_t smem_bytes_v3() {
 // compiled without any mirror code, so the benchmark path's code is untouched)
 template <int NP_, bool MIR>
 __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a) {
+    // (no early trigger: the macro sweep's CTAs would sit on the SMs while
+    // the bands finish; M32_PDL_TRIGGER=1 measures that variant)
+    pdl_enter<M32_PDL_TRIGGER != 0>();
     static_assert(NP_ == 4, "the TMEM ring is laid out for 4 node pairs per thread");
     constexpr int NT_ = 512 / NP_;       // threads per CTA
     constexpr int KS = 32 / NP_;         // k step between a thread's node pairs
@@ -1025,6 +1031,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
 // extend_maxwellian_2d 304-340).  One CTA per strip cell; faces laid out
 // left (by), right (by), bottom (bx), top (bx).
 __global__ void __launch_bounds__(128) k_wall_ghat(MicroArgs a, double* out) {
+    pdl_enter();
     __shared__ double sh[32];
     const Geometry& g = a.g;
     if (*a.err != kNoError) return;

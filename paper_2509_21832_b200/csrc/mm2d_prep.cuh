@@ -321,6 +321,7 @@ __device__ __forceinline__ void nb_prims(const PrepArgs& a, int i, int j, double
 // One thread per ring cell; each owned cell re-derives its four neighbours'
 // primitives from Q (the reference's extend + centred difference).
 __global__ void k_prep(PrepArgs a) {
+    pdl_enter();
     const Geometry& g = a.g;
     if (*a.err != kNoError) return;
     const int n = (g.bx + 2) * (g.by + 2);
@@ -351,6 +352,7 @@ __device__ __forceinline__ int prep_tiles(const Geometry& g) {
 }
 
 __global__ void __launch_bounds__(PT_THREADS) k_prep_tiled(PrepArgs a) {
+    pdl_enter();
     const Geometry& g = a.g;
     if (*a.err != kNoError) return;
     __shared__ double sw[3][PT_I + 2][PT_J + 2];
