@@ -344,7 +344,10 @@ __global__ void k_prep(PrepArgs a) {
 // shared memory, then every cell of the tile reads its neighbours from
 // there: one Q load and one primitive evaluation per cell instead of five,
 // and the same prims_fast arithmetic, so the CellPar bits are unchanged.
-constexpr int PT_I = 8, PT_J = 32, PT_THREADS = PT_I * PT_J;
+#ifndef MM2D_PREP_TI
+#define MM2D_PREP_TI 8   // tile rows (warps per CTA)
+#endif
+constexpr int PT_I = MM2D_PREP_TI, PT_J = 32, PT_THREADS = PT_I * PT_J;
 constexpr size_t kPrepStageBytes = sizeof(CellPar) * PT_THREADS;
 
 __device__ __forceinline__ int prep_tiles(const Geometry& g) {
