@@ -345,7 +345,7 @@ __global__ void k_prep(PrepArgs a) {
 // there: one Q load and one primitive evaluation per cell instead of five,
 // and the same prims_fast arithmetic, so the CellPar bits are unchanged.
 #ifndef MM2D_PREP_TI
-#define MM2D_PREP_TI 8   // tile rows (warps per CTA)
+#define MM2D_PREP_TI 4   // tile rows (warps per CTA); 4 measured faster than 8
 #endif
 constexpr int PT_I = MM2D_PREP_TI, PT_J = 32, PT_THREADS = PT_I * PT_J;
 constexpr size_t kPrepStageBytes = sizeof(CellPar) * PT_THREADS;
