@@ -96,6 +96,9 @@ int mm2d_create(const mm2d_config *cfg, mm2d_ctx **out);
 int mm2d_destroy(mm2d_ctx *ctx);
 const char *mm2d_last_error(mm2d_ctx *ctx);
 int mm2d_version(void);
+/* version of the fused micro kernel (k_micro32); ties committed ncu
+ * captures (profiles/micro_traffic.json) to the code that produced them */
+int mm2d_kernel_version(void);
 
 /* local block geometry of this rank: (bx, by) cells starting at (i0, j0) */
 int mm2d_block(mm2d_ctx *ctx, int *bx, int *by, int *i0, int *j0);
@@ -218,10 +221,11 @@ int mm2d_k_project_field_1d(int nx, int nv, const double *F, const double *M,
                             const double *rho, const double *u, const double *T,
                             const double *v, double dv, double *out, void *stream);
 
-/* per-kernel device time of one step on the attached/owned state: runs
- * nrep steps without a graph, bracketing every kernel with CUDA events on
- * the stream it is launched on, and returns the mean milliseconds per launch
- * in ms[0..6] = fill_qring, prep, micro, fill_hring, macro_x, macro_y, h_soa */
+/* per-kernel device time on the attached/owned state: captures nrep steps
+ * as ONE CUDA graph (the path mm2d_run replays) with external event-record
+ * nodes around every kernel, launches it once and returns the mean
+ * milliseconds per launch in ms[0..6] = (none), prep, micro, (none),
+ * macro_x, macro_y, (none) */
 int mm2d_time_kernels(mm2d_ctx *ctx, double dt, int nrep, double *ms);
 
 /* device launches counted since the last reset (bench.py's gpu_launches) */

@@ -70,6 +70,7 @@ class Config1D(C.Structure):
 # exports exactly these names
 SIGNATURES = {
     "mm2d_version": (C.c_int, []),
+    "mm2d_kernel_version": (C.c_int, []),
     "mm2d_create": (C.c_int, [C.POINTER(Config), C.POINTER(_vp)]),
     "mm2d_destroy": (C.c_int, [_vp]),
     "mm2d_last_error": (C.c_char_p, [_vp]),

@@ -149,12 +149,13 @@ struct Args1 {
     const double* v3;     // (nv) v^3 (host pow, as numpy's v**3)
     const double* src;    // (nx, nv) projected micro source or null
     const double* qsrc;   // (nx, 3) macro source or null
-    unsigned long long* err;   // [0] key, [1] failing Q pointer
+    unsigned long long* err;   // [0] merged key, [1] failing Q pointer, [2] steps done,
+                               // [3] key raised by k1_micro (merged into [0] by k1_macro)
     double dt;
 };
 
 __device__ __forceinline__ void flag1(const Args1& a, int stage, int cell) {
-    atomicMin(a.err, err_key(0, stage, (unsigned long long)cell));
+    atomicMin(a.err + 3, err_key(0, stage, (unsigned long long)cell));   // k1_micro's own word
     a.err[1] = (unsigned long long)(size_t)a.Q;
 }
 
@@ -163,7 +164,7 @@ __device__ __forceinline__ void flag1(const Args1& a, int stage, int cell) {
 __global__ void k1_micro(Args1 a) {
     __shared__ double sh[4][32];
     const Geo1& g = a.g;
-    if (*a.err != kNoError) return;
+    if (*(volatile const unsigned long long*)a.err != kNoError) return;   // earlier launches only
     const int i = blockIdx.x;
     const int nv = g.nv;
     const Prim1 P = prim1(a.Q + 3 * i);
@@ -235,7 +236,7 @@ __global__ void k1_micro(Args1 a) {
 // macro_step_1d (macro1d.py:78-92): flux differences, heat flux, source
 __global__ void k1_macro(Args1 a) {
     const Geo1& g = a.g;
-    if (*a.err != kNoError) return;
+    if (err_gate(a.err, 3)) return;   // k1_micro of this step or an earlier failure
     const double r = a.dt / g.dx;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.nx; i += gridDim.x * blockDim.x) {
         const int il = nb1(g, i - 1), ir = nb1(g, i + 1);

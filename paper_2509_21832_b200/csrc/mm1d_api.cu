@@ -159,7 +159,7 @@ extern "C" int mm1d_create(const mm1d_config* cfg, mm1d_ctx** out) {
         cudaMalloc(&ctx->d_err, sizeof(unsigned long long) * 4) != cudaSuccess ||
         cudaMemcpy(ctx->d_v, v, sizeof(double) * c.nv, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(ctx->d_v3, v3, sizeof(double) * c.nv, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemset(ctx->d_err, 0xff, sizeof(unsigned long long)) != cudaSuccess)
+        cudaMemset(ctx->d_err, 0xff, sizeof(unsigned long long) * 4) != cudaSuccess)
         rc = MM2D_ERR_INTERNAL;
     delete[] v;
     delete[] v3;
@@ -335,8 +335,9 @@ extern "C" int mm1d_check(mm1d_ctx* ctx, int* kind, int* i, double* value) {
     if (!ctx) return MM2D_ERR_CONFIG;
     CK1(cudaSetDevice(ctx->dev));
     CK1(cudaDeviceSynchronize());
-    unsigned long long w[2];
+    unsigned long long w[4];
     CK1(cudaMemcpy(w, ctx->d_err, sizeof(w), cudaMemcpyDeviceToHost));
+    if (w[3] < w[0]) w[0] = w[3];
     if (w[0] == kNoError) return MM2D_OK;
     const int stage = (int)((w[0] >> 36) & 0xf);
     const int cell = (int)(w[0] & ((1ull << 36) - 1));
@@ -347,6 +348,7 @@ extern "C" int mm1d_check(mm1d_ctx* ctx, int* kind, int* i, double* value) {
     CK1(cudaMemcpy(&v, d_v, sizeof(double), cudaMemcpyDeviceToHost));
     cudaFree(d_v);
     CK1(cudaMemset(ctx->d_err, 0xff, sizeof(unsigned long long)));
+    CK1(cudaMemset(ctx->d_err + 3, 0xff, sizeof(unsigned long long)));
     if (kind) *kind = stage == E1_DENSITY ? MM1D_STATE_DENSITY : MM1D_STATE_TEMPERATURE;
     if (i) *i = cell;
     if (value) *value = v;

@@ -98,7 +98,9 @@ __global__ void __launch_bounds__(512) k1_resident(Res1 a) {
     // ---- prologue: load the state, primitives (and their check) of Q^0 ----
     for (int n = tid; n < cnt * nv; n += blockDim.x) Gs0[n] = a.G[(size_t)c0 * nv + n];
     for (int n = tid; n < cnt * 3; n += blockDim.x) Qs[n] = a.Q[(size_t)c0 * 3 + n];
-    if (tid == 0) *flag = (*(volatile unsigned long long*)a.err != kNoError) ? 1 : 0;
+    if (tid == 0)
+        *flag = (*(volatile unsigned long long*)a.err != kNoError ||
+                 *(volatile unsigned long long*)(a.err + 3) != kNoError) ? 1 : 0;
     double vk[NJ], v3k[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {

@@ -45,7 +45,9 @@ struct mm2d_ctx {
     double* d_Qr = nullptr;
     double* d_Hr = nullptr;
     double* d_Qx = nullptr;
-    unsigned long long* d_err = nullptr;   // [0] key, [1..4] iso maxima
+    unsigned long long* d_err = nullptr;   // ErrWord layout (mm2d_common.cuh) + [8] error value
+    unsigned long long* h_err = nullptr;   // pinned read-back of the 9 words
+    cudaStream_t last_s = nullptr;         // stream of the last enqueued step (mm2d_check syncs it)
     // halo buffers for the micro field (multi-rank only)
     double* d_gh[4] = {nullptr, nullptr, nullptr, nullptr};
     double* d_wallg = nullptr;     // wall-strip targets (fast kernel)
@@ -79,6 +81,7 @@ struct mm2d_ctx {
     int halo_cells[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     double* hsend[3][8] = {};
     double* hrecv[3][8] = {};
+    int sms = 148;                 // multiprocessors of the context's device
     std::string err;
 };
 
@@ -161,6 +164,8 @@ static std::vector<int> pick_bands(int bx, int by, long long slots, int ly) {
 }
 
 extern "C" int mm2d_version(void) { return 1; }
+
+extern "C" int mm2d_kernel_version(void) { return M32_KERNEL_VERSION; }
 
 extern "C" const char* mm2d_last_error(mm2d_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 
@@ -371,10 +376,20 @@ extern "C" int mm2d_create(const mm2d_config* cfg, mm2d_ctx** out) {
     CK(cudaMemset(ctx->d_Qr, 0, sizeof(double) * 6 * ring));
     CK(cudaMemset(ctx->d_Hr, 0, sizeof(double) * 4 * ring));
     CK(cudaMemset(ctx->d_Qx, 0, sizeof(double) * 6 * ring));
-    CK(cudaMalloc(&ctx->d_err, sizeof(unsigned long long) * 8));
+    CK(cudaMalloc(&ctx->d_err, sizeof(unsigned long long) * (EW_N + 1)));
+    CK(cudaMallocHost(&ctx->h_err, sizeof(unsigned long long) * (EW_N + 1)));
     {
-        unsigned long long init[8] = {kNoError, 0, 0, 0, 0, 0, 0, 0};
+        unsigned long long init[EW_N + 1] = {kNoError, 0, 0, 0, 0, kNoError, kNoError, kNoError, 0};
         CK(cudaMemcpy(ctx->d_err, init, sizeof(init), cudaMemcpyHostToDevice));
+    }
+    // the launch attribute the tiled prep needs, set once here (outside any
+    // stream capture) instead of on the launch path
+    CK(cudaFuncSetAttribute(k_prep_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kPrepStageBytes));
+    {
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->dev));
+        ctx->sms = sms > 0 ? sms : 148;
     }
     const size_t Vs = (size_t)V;
     for (int f = 0; f < 4; ++f) {
@@ -419,6 +434,7 @@ extern "C" int mm2d_destroy(mm2d_ctx* ctx) {
     cudaFree(ctx->d_zero);
     cudaFree(ctx->d_v1); cudaFree(ctx->d_v2); cudaFree(ctx->d_P); cudaFree(ctx->d_Qr);
     cudaFree(ctx->d_Hr); cudaFree(ctx->d_Qx); cudaFree(ctx->d_err);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return MM2D_OK;
@@ -455,8 +471,13 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
                         int phases = 3, int part = 0, int mode = 0) {
     // part: micro CTAs launched (0 all, 1 those that read no received G halo,
     // 2 the others); mode: 0 prep + micro, 1 prep only, 2 micro only
+    // event marks: plain records, or external record nodes when capturing
+    // (mm2d_time_kernels times the captured graph itself)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (ev) CK(cudaStreamIsCapturing(s, &cap));
 #define MARK(q) \
-    if (ev) CK(cudaEventRecord(ev[q], s))
+    if (ev) CK(cudaEventRecordWithFlags(ev[q], s, cap == cudaStreamCaptureStatusActive ? \
+                                                       cudaEventRecordExternal : cudaEventRecordDefault))
     const Geometry& g = ctx->g;
     const mm2d_config& c = ctx->cfg;
     const long long ring = (long long)(g.bx + 2) * (g.by + 2);
@@ -470,6 +491,7 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     }
     ctx->last_dt = dt;
     ctx->last_Qout = Qout;
+    ctx->last_s = s;
     if (phases & 1) {
     MARK(0);
     MARK(1);   // (the Q ring is filled by k_prep)
@@ -490,16 +512,8 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
 #if MM2D_PREP_TILED
         {
             const int nt = ((g.bx + 2 + PT_I - 1) / PT_I) * ((g.by + 2 + PT_J - 1) / PT_J);
-            static std::atomic<bool> attr[64];   // per device: the attribute is per context
-            int dev = 0;
-            CK(cudaGetDevice(&dev));
-            if (dev < 0 || dev >= 64 || !attr[dev].load()) {
-                CK(cudaFuncSetAttribute(k_prep_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kPrepStageBytes));
-                if (dev >= 0 && dev < 64) attr[dev] = true;
-            }
-            CK(launch_pdl(k_prep_tiled, dim3(std::max(1, std::min(nt, 148 * 8))), dim3(PT_THREADS),
-                          kPrepStageBytes, s, pa));
+            CK(launch_pdl(k_prep_tiled, dim3(std::max(1, std::min(nt, ctx->sms * 8))),
+                          dim3(PT_THREADS), kPrepStageBytes, s, pa));
         }
 #else
         CK(launch_pdl(k_prep, dim3(grid_for(ring, 128)), dim3(128), 0, s, pa));
@@ -707,6 +721,7 @@ extern "C" int mm2d_run(mm2d_ctx* ctx, double dt, int nsteps) {
     }
     for (int n = 0; n < nsteps; ++n) {
         CK(cudaGraphLaunch(ctx->gexec[ctx->cur], ctx->stream));
+        ctx->last_s = ctx->stream;
         ctx->cur ^= 1;
         g_launches += ctx->launches_per_step;
     }
@@ -720,29 +735,41 @@ extern "C" int mm2d_run(mm2d_ctx* ctx, double dt, int nsteps) {
 extern "C" int mm2d_time_kernels(mm2d_ctx* ctx, double dt, int nrep, double* ms) {
     if (!ctx || !ctx->d_Qs[0] || !ms || nrep < 1) return fail_cfg(ctx, "time_kernels needs state");
     CK(cudaSetDevice(ctx->dev));
-    cudaEvent_t ev[8];
-    for (int q = 0; q < 8; ++q) CK(cudaEventCreate(&ev[q]));
+    std::vector<cudaEvent_t> ev((size_t)8 * nrep, nullptr);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    ctx->counting = false;
+    int cur = ctx->cur, rc = MM2D_OK;
+    for (int r = 0; r < nrep && rc == MM2D_OK; ++r, cur ^= 1)
+        rc = enqueue_step(ctx, ctx->d_Qs[cur], ctx->d_Gs[cur], dt, ctx->d_Qs[1 - cur],
+                          ctx->d_Gs[1 - cur], ctx->d_Hsoa, 0, nullptr, nullptr, nullptr,
+                          ctx->stream, &ev[(size_t)8 * r]);
+    ctx->counting = true;
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (rc) return rc;
+    CK(e);
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
     if (ctx->have_user_stream) {
-        CK(cudaEventRecord(ev[0], ctx->user_stream));
-        CK(cudaStreamWaitEvent(ctx->stream, ev[0], 0));
+        CK(cudaEventRecord(ctx->ev_in, ctx->user_stream));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in, 0));
     }
-    for (int r = 0; r < nrep; ++r) {
-        const int p = ctx->cur;
-        int rc = enqueue_step(ctx, ctx->d_Qs[p], ctx->d_Gs[p], dt, ctx->d_Qs[1 - p],
-                              ctx->d_Gs[1 - p], ctx->d_Hsoa, 0, nullptr, nullptr, nullptr,
-                              ctx->stream, ev);
-        if (rc) return rc;
-        ctx->cur ^= 1;
-        CK(cudaEventSynchronize(ev[7]));
+    CK(cudaGraphLaunch(exec, ctx->stream));
+    ctx->last_s = ctx->stream;
+    ctx->cur = cur;
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaGraphExecDestroy(exec);
+    for (int r = 0; r < nrep; ++r)
         for (int q = 0; q < 7; ++q) {
             float t = 0.f;
-            CK(cudaEventElapsedTime(&t, ev[q], ev[q + 1]));
+            CK(cudaEventElapsedTime(&t, ev[(size_t)8 * r + q], ev[(size_t)8 * r + q + 1]));
             acc[q] += t;
         }
-    }
     for (int q = 0; q < 7; ++q) ms[q] = acc[q] / nrep;
-    for (int q = 0; q < 8; ++q) cudaEventDestroy(ev[q]);
+    for (auto& x : ev) cudaEventDestroy(x);
     return MM2D_OK;
 }
 
@@ -873,9 +900,13 @@ __global__ void k_err_value(Geometry g, int stage, int i, int j, const double* Q
 extern "C" int mm2d_check(mm2d_ctx* ctx, int* kind, int* i, int* j, double* value) {
     if (!ctx) return MM2D_ERR_CONFIG;
     CK(cudaSetDevice(ctx->dev));
-    CK(cudaDeviceSynchronize());
-    unsigned long long key;
-    CK(cudaMemcpy(&key, ctx->d_err, sizeof(key), cudaMemcpyDeviceToHost));
+    // stream-scoped: wait for the context's last step only, not the device
+    cudaStream_t s = ctx->last_s;
+    unsigned long long* h = ctx->h_err;
+    CK(cudaMemcpyAsync(h, ctx->d_err, sizeof(unsigned long long) * EW_N, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    unsigned long long key = h[EW_E];
+    for (int w : {EW_PREP, EW_MX, EW_MY}) key = h[w] < key ? h[w] : key;
     if (key == kNoError) return MM2D_OK;
     const int stage = (int)((key >> 36) & 0xf);
     const unsigned long long cell = key & ((1ull << 36) - 1);
@@ -886,20 +917,19 @@ extern "C" int mm2d_check(mm2d_ctx* ctx, int* kind, int* i, int* j, double* valu
         k = MM2D_STATE_DENSITY;
     else if (stage == ES_MOD_SPD)
         k = MM2D_STATE_MODIFIED;
-    double* d_v;
-    double v = 0.0;
-    CK(cudaMalloc(&d_v, sizeof(double)));
+    double* d_v = reinterpret_cast<double*>(ctx->d_err + EW_N);
     const mm2d_config& c = ctx->cfg;
-    k_err_value<<<1, 1>>>(ctx->g, stage, li, lj, ctx->d_Qr, ctx->d_Qx, ctx->last_Qout, c.nu,
-                          c.tau_kind, c.tau_value, ctx->last_dt, c.eps, d_v);
-    CK(cudaMemcpy(&v, d_v, sizeof(double), cudaMemcpyDeviceToHost));
-    cudaFree(d_v);
-    // report once: the next step starts from a clean error word (the
-    // reference raises per call)
-    {
-        const unsigned long long none = kNoError;
-        CK(cudaMemcpy(ctx->d_err, &none, sizeof(none), cudaMemcpyHostToDevice));
-    }
+    k_err_value<<<1, 1, 0, s>>>(ctx->g, stage, li, lj, ctx->d_Qr, ctx->d_Qx, ctx->last_Qout, c.nu,
+                                c.tau_kind, c.tau_value, ctx->last_dt, c.eps, d_v);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h + EW_N, d_v, sizeof(double), cudaMemcpyDeviceToHost, s));
+    // report once: the next step starts from clean error words (the
+    // reference raises per call); kNoError is all-ones bytes
+    CK(cudaMemsetAsync(ctx->d_err + EW_E, 0xff, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(ctx->d_err + EW_PREP, 0xff, sizeof(unsigned long long) * 3, s));
+    CK(cudaStreamSynchronize(s));
+    double v;
+    memcpy(&v, h + EW_N, sizeof(double));
     if (kind) *kind = k;
     if (i) *i = gi;
     if (j) *j = gj;

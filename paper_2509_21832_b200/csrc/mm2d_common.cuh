@@ -55,6 +55,32 @@ __host__ __device__ inline unsigned long long err_key(unsigned step, unsigned st
 }
 constexpr unsigned long long kNoError = ~0ull;
 
+// Error words of a context (8 x u64): [0] E, the merged key of every
+// completed kernel; [1..4] isotropy maxima; [5] R_prep, [6] R_mx, [7] R_my,
+// the keys raised by k_prep, k_macro_x and k_macro_y.  A kernel raises into
+// its OWN word and skips its work only on keys raised by earlier launches:
+// its gate is min(E, R of the kernel before it), both of which are stable
+// while it runs, so every CTA of one launch takes the same decision and a
+// launch never stops itself part-way (the minimum over all its offending
+// cells is what the reference's first-failure order asks for).  The kernel
+// also folds that predecessor word into E (atomicMin is idempotent), so E
+// accumulates every failure one launch later; mm2d_check reads min(E, R_*).
+enum ErrWord { EW_E = 0, EW_ISO = 1, EW_PREP = 5, EW_MX = 6, EW_MY = 7, EW_N = 8 };
+
+__device__ __forceinline__ bool err_gate(unsigned long long* w, int prev) {
+    const unsigned long long rp = *(volatile const unsigned long long*)(w + prev);
+    if (rp != kNoError && threadIdx.x == 0 && threadIdx.y == 0 && blockIdx.x == 0 &&
+        blockIdx.y == 0)
+        atomicMin(w + EW_E, rp);
+    const unsigned long long e = *(volatile const unsigned long long*)(w + EW_E);
+    return (e < rp ? e : rp) != kNoError;
+}
+// read-only form for kernels that raise nothing (the micro kernels)
+__device__ __forceinline__ bool err_pending(const unsigned long long* w, int prev) {
+    const unsigned long long rp = w[prev], e = w[EW_E];
+    return (e < rp ? e : rp) != kNoError;
+}
+
 // Per-ring-cell parameters produced by the prep kernel (all from Q^n).
 struct __align__(16) CellPar {
     double rho, u1, u2, T;           // 0-3   primitives (gas_state.py:93-108)

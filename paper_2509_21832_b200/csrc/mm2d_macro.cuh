@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(MX_TJ * (MX_TI + 2)) k_macro_x(MacroArgs a) {
     pdl_enter();
     __shared__ double sL[MX_TI + 2][6][MX_TJ], sR[MX_TI + 2][6][MX_TJ];
     const Geometry& g = a.g;
-    if (*a.err != kNoError) return;
+    if (err_gate(a.err, EW_PREP)) return;
     const int jlo = g.qylo == GM_HALO ? -1 : 0;
     const int jhi = g.qyhi == GM_HALO ? g.by : g.by - 1;
     const int lane = threadIdx.x, r = threadIdx.y;
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(MX_TJ * (MX_TI + 2)) k_macro_x(MacroArgs a) {
         if (bs) {
             const unsigned long long gcell =
                 (unsigned long long)(g.i0 + i) * g.ny + (unsigned long long)(g.j0 + j);
-            atomicMin(a.err, err_key(a.step, bs == 1 ? ES_XS_RHO : ES_XS_SPD, gcell));
+            atomicMin(a.err + EW_MX, err_key(a.step, bs == 1 ? ES_XS_RHO : ES_XS_SPD, gcell));
         }
     }
     double* o = a.Qx + 6 * ring_index(g, i, j);
@@ -203,7 +203,7 @@ constexpr int MY_OUT = 30;
 __global__ void __launch_bounds__(128) k_macro_y(MacroArgs a) {
     pdl_enter();
     const Geometry& g = a.g;
-    if (*a.err != kNoError) return;
+    if (err_gate(a.err, EW_MX)) return;
     const int lane = threadIdx.x & 31;
     const int i = blockIdx.y * 4 + (threadIdx.x >> 5);
     if (i >= g.bx) return;                       // warp-uniform
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(128) k_macro_y(MacroArgs a) {
         (unsigned long long)(g.i0 + i) * g.ny + (unsigned long long)(g.j0 + j);
     {
         const int bs = bad_state(qc);
-        if (bs) atomicMin(a.err, err_key(a.step, bs == 1 ? ES_YS_RHO : ES_YS_SPD, gcell));
+        if (bs) atomicMin(a.err + EW_MY, err_key(a.step, bs == 1 ? ES_YS_RHO : ES_YS_SPD, gcell));
     }
     double q3[6];
 #pragma unroll
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(128) k_macro_y(MacroArgs a) {
     const int bs3 = bad_state(q3);
     if (bs3) {
         // keep Q*** so the host can report the offending value
-        atomicMin(a.err, err_key(a.step, bs3 == 1 ? ES_RL_RHO : ES_RL_SPD, gcell));
+        atomicMin(a.err + EW_MY, err_key(a.step, bs3 == 1 ? ES_RL_RHO : ES_RL_SPD, gcell));
         for (int m = 0; m < 6; ++m) qo[m] = q3[m];
     } else {
         relax_cell(a, q3, qo);

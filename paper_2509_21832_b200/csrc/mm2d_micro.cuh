@@ -247,7 +247,7 @@ template <int NE, int BX, bool FAST>
 __global__ void __launch_bounds__(256) k_micro(MicroArgs a) {
     extern __shared__ __align__(16) double smem[];
     const Geometry& g = a.g;
-    if (*a.err != kNoError) return;
+    if (err_pending(a.err, EW_PREP)) return;
     const int NT = blockDim.x;
     const int nwarps = NT >> 5;
     const int tid = threadIdx.x;

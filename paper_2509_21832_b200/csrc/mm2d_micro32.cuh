@@ -28,6 +28,12 @@
 #include "mm2d_common.cuh"
 #include "mm2d_micro.cuh"
 
+// version of this kernel: bump on every change that alters its code, so
+// committed ncu captures (profiles/micro_traffic.json) stay tied to it
+#ifndef M32_KERNEL_VERSION
+#define M32_KERNEL_VERSION 26
+#endif
+
 #ifndef MICRO32_MINB
 #define MICRO32_MINB 4   // resident CTAs per SM the register budget is sized for: 4 x 128
                          // threads at 128 registers and 55 KB of shared memory (the K-table
@@ -631,7 +637,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     };
 
     if (computes(j0s - 1)) prefetch(j0s - 1, std::false_type());
-    if (*a.err != kNoError) {
+    if (err_pending(a.err, EW_PREP)) {
         // an earlier stage failed: leave the step's inputs untouched, after
         // the copies in flight have landed
         cp_async_wait_all();
@@ -1034,7 +1040,7 @@ __global__ void __launch_bounds__(128) k_wall_ghat(MicroArgs a, double* out) {
     pdl_enter();
     __shared__ double sh[32];
     const Geometry& g = a.g;
-    if (*a.err != kNoError) return;
+    if (err_pending(a.err, EW_PREP)) return;
     const int e = blockIdx.x;
     int f, i, j;
     if (e < g.by) { f = 0; i = 0; j = e; }

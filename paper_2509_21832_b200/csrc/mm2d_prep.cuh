@@ -79,33 +79,6 @@ __device__ __forceinline__ bool load_ring_q(const Geometry& g, const double* __r
     return own_copy;
 }
 
-// Fill the ghost ring of Qr from the owned block Q (bx, by, 6).  Cells that
-// resolve to themselves as received halo data are left untouched.
-__global__ void k_fill_qring(Geometry g, const double* __restrict__ Q, double* __restrict__ Qr,
-                             const unsigned long long* __restrict__ err) {
-    if (*err != kNoError) return;   // keep the failing step's inputs intact
-    const int n = (g.bx + 2) * (g.by + 2);
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
-        int si, sj, flip;
-        const int rs = resolve_ring(g.bx, g.by, g.qxlo, g.qxhi, g.qylo, g.qyhi, i, j, si, sj, flip);
-        double* dst = Qr + 6 * t;
-        if (rs == RS_INTERIOR) {
-            const double* src = Q + 6 * ((size_t)si * g.by + sj);
-#pragma unroll
-            for (int c = 0; c < 6; ++c) dst[c] = flip ? q_mirror_sign(c, flip) * src[c] : src[c];
-        } else if (rs == RS_RING) {
-            if (si == i && sj == j) continue;   // received directly
-            const double* src = Qr + 6 * ring_index(g, si, sj);
-#pragma unroll
-            for (int c = 0; c < 6; ++c) dst[c] = flip ? q_mirror_sign(c, flip) * src[c] : src[c];
-        } else {
-#pragma unroll
-            for (int c = 0; c < 6; ++c) dst[c] = 0.0;
-        }
-    }
-}
-
 // Fill the ghost ring of Hr (owned part written by the micro kernel).
 // Heat ghosts: periodic wrap, extrapolate copy, wall zero, i.e. the rules of
 // interface_heat_2d (boundary.py:224-241): the interface value is the mean
@@ -152,7 +125,7 @@ struct PrepArgs {
     const double* Q;              // owned block (bx, by, 6)
     double* Qr;                   // ring, written here (received halo cells kept)
     CellPar* P;
-    unsigned long long* err;      // sticky error key
+    unsigned long long* err;      // the context's error words (ErrWord)
     unsigned long long* iso;      // [4]: max|m11-T|, max|m12|, max|m22-T|, max T (bit patterns)
     double dt, eps, nu, dv;
     int tau_kind;
@@ -232,13 +205,13 @@ __device__ __forceinline__ void prep_cell(const PrepArgs& a, int t, int i, int j
         rho = q[0];
         const unsigned long long gcell =
             (unsigned long long)(g.i0 + i) * g.ny + (unsigned long long)(g.j0 + j);
-        if (own && !(rho > 0.0)) atomicMin(a.err, err_key(a.step, ES_PRIM_RHO, gcell));
+        if (own && !(rho > 0.0)) atomicMin(a.err + EW_PREP, err_key(a.step, ES_PRIM_RHO, gcell));
         prims_of(q, rho, u1, u2, t11, t12, t22);
         const double T = 0.5 * (t11 + t22);
         if (own) {
             const double tol = 1e-14 * (t11 + t22);
             const double det = t11 * t22 - t12 * t12;
-            if ((t11 <= tol) || (det <= tol * tol)) atomicMin(a.err, err_key(a.step, ES_PRIM_SPD, gcell));
+            if ((t11 <= tol) || (det <= tol * tol)) atomicMin(a.err + EW_PREP, err_key(a.step, ES_PRIM_SPD, gcell));
         }
         P.rho = rho; P.u1 = u1; P.u2 = u2; P.T = T;
         P.t11 = t11; P.t12 = t12; P.t22 = t22;
@@ -275,7 +248,7 @@ __device__ __forceinline__ void prep_cell(const PrepArgs& a, int t, int i, int j
             if (own) {
                 const double tol = 1e-14 * (m11 + m22);
                 if ((m11 <= tol) || (det <= tol * tol))
-                    atomicMin(a.err, err_key(a.step, ES_MOD_SPD, gcell));
+                    atomicMin(a.err + EW_PREP, err_key(a.step, ES_MOD_SPD, gcell));
                 if (a.eps < 1e-10) {
                     atomic_max_pos(&a.iso[0], fabs(m11 - T));
                     atomic_max_pos(&a.iso[1], fabs(m12));
@@ -323,7 +296,7 @@ __device__ __forceinline__ void nb_prims(const PrepArgs& a, int i, int j, double
 __global__ void k_prep(PrepArgs a) {
     pdl_enter();
     const Geometry& g = a.g;
-    if (*a.err != kNoError) return;
+    if (err_gate(a.err, EW_MY)) return;   // failed in an earlier launch
     const int n = (g.bx + 2) * (g.by + 2);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
         const int i = t / (g.by + 2) - 1, j = t % (g.by + 2) - 1;
@@ -357,7 +330,7 @@ __device__ __forceinline__ int prep_tiles(const Geometry& g) {
 __global__ void __launch_bounds__(PT_THREADS) k_prep_tiled(PrepArgs a) {
     pdl_enter();
     const Geometry& g = a.g;
-    if (*a.err != kNoError) return;
+    if (err_gate(a.err, EW_MY)) return;   // failed in an earlier launch
     __shared__ double sw[3][PT_I + 2][PT_J + 2];
     extern __shared__ double stage[];   // [PT_THREADS][32] CellPar staging (swizzled)
     const int ntj = (g.by + 2 + PT_J - 1) / PT_J;

@@ -224,7 +224,10 @@ def get_solver(mesh, bc, eps, model, device=None) -> Solver2D:
     if key is not None:
         _CACHE[key] = s
         while len(_CACHE) > _CACHE_SIZE:
-            _CACHE.popitem(last=False)[1].close()
+            # drop only the cache's reference: states returned by step_2d /
+            # run_2d keep their solver (and its pending error) alive, and
+            # __del__ frees the context once nothing refers to it
+            _CACHE.popitem(last=False)
     return s
 
 
@@ -301,8 +304,10 @@ def step_2d(state, mesh, bc, eps, model, dt, micro_source=None, macro_source=Non
         st = state
     else:  # the reference's own State2D (or any object with t, Q, G)
         st = State2D(state.t, state.Q, state.G)
-    if st._solver is not None:
-        st._solver.check()
+    # no host synchronisation here: a state stepped on the same context keeps
+    # any pending device error sticky (the step's kernels skip their work and
+    # the error is raised when the host next reads .Q / .G or calls check());
+    # a state from another context is checked in device_arrays
     Q, G = st.device_arrays(solver)
     src = qsrc = None
     if micro_source is not None or macro_source is not None:

@@ -176,7 +176,8 @@ def get_solver_1d(mesh, bc, eps, model, device=None) -> Solver1D:
     if key is not None:
         _CACHE[key] = s
         while len(_CACHE) > 4:
-            _CACHE.popitem(last=False)[1].close()
+            # drop only the cache's reference: live states keep their solver
+            _CACHE.popitem(last=False)
     return s
 
 
@@ -238,8 +239,8 @@ def step_1d(state, mesh, bc, eps, model, dt, micro_source=None, macro_source=Non
     """
     solver = get_solver_1d(mesh, bc, eps, model)
     st = state if isinstance(state, State1D) else State1D(state.t, state.Q, state.G)
-    if st._solver is not None:
-        st._solver.check()
+    # no per-step host sync: errors stay sticky on the context and surface
+    # when the host reads the state (device_arrays checks a foreign context)
     Q, G = st.device_arrays(solver)
     x = cell_centers(mesh.space[0])
     src = micro_source(st.t, x, solver.v) if micro_source is not None else None

@@ -59,19 +59,19 @@ def cases_2d():
         # term is live, nonzero micro field
         ("wave_periodic", dict(nx=12, ny=12, vx=(-7.0, 7.0, 8), vy=(-7.0, 7.0, 8),
                                faces=("periodic",) * 4, kind="esbgk_2d", nu=-0.5,
-                               eps=0.1, ic="wave", gscale=0.01, steps=(1, 10))),
+                               eps=0.1, ic="wave", gscale=0.01, steps=(1, 10, 100))),
         # C3-like four-quadrant Riemann, all faces extrapolate, nx != ny,
         # non-square velocity grid
         ("riemann_extrap", dict(nx=16, ny=12, vx=(-8.0, 8.0, 8), vy=(-8.0, 8.0, 6),
                                 faces=("extrapolate",) * 4, kind="esbgk_2d", nu=-0.5,
-                                eps=1e-2, ic="riemann", gscale=0.0, steps=(1, 10))),
+                                eps=1e-2, ic="riemann", gscale=0.0, steps=(1, 10, 100))),
         ("riemann_extrap_eps1e-3", dict(nx=12, ny=12, vx=(-8.0, 8.0, 8), vy=(-8.0, 8.0, 8),
                                         faces=("extrapolate",) * 4, kind="esbgk_2d", nu=-0.5,
                                         eps=1e-3, ic="riemann", gscale=0.0, steps=(1, 10))),
         # C4-like closed box with diffuse walls on all faces
         ("box_walls", dict(nx=12, ny=12, vx=(-8.0, 8.0, 8), vy=(-8.0, 8.0, 8),
                            faces=({"wall": [1.0, 0.0]},) * 4, kind="esbgk_2d", nu=-0.5,
-                           eps=5e-2, ic="bump", gscale=0.005, steps=(1, 10))),
+                           eps=5e-2, ic="bump", gscale=0.005, steps=(1, 10, 100))),
         # lid-driven cavity (reference default case shape), sliding top lid
         ("cavity_lid", dict(nx=10, ny=10, vx=(-5.0, 5.0, 6), vy=(-5.0, 5.0, 6),
                             faces=({"wall": [1.0, 0.0]}, {"wall": [1.0, 0.0]},
@@ -101,6 +101,21 @@ def cases_2d():
         ("box_v1024", dict(nx=6, ny=6, vx=(-8.0, 8.0, 32), vy=(-8.0, 8.0, 32),
                            faces=({"wall": [1.0, 0.0]},) * 4, kind="esbgk_2d", nu=-0.5,
                            eps=5e-2, ic="bump", gscale=0.005, steps=(1, 3))),
+        # (round 2) the eps < 1e-10 isotropy guard (micro2d.py:96) on the
+        # benchmark velocity grid, i.e. on the specialised 32 x 32 kernel:
+        # isotropic tensor -> the Gaussian term is skipped ...
+        ("iso_v1024_eps1e-12", dict(nx=6, ny=6, vx=(-7.0, 7.0, 32), vy=(-7.0, 7.0, 32),
+                                    faces=("periodic",) * 4, kind="esbgk_2d", nu=-0.5,
+                                    eps=1e-12, ic="iso", gscale=0.0, steps=(1,))),
+        # (only one step: after it the physical anisotropy is O(eps) = 1e-12,
+        # at the guard's own 1e-13 max T threshold, so whether later steps
+        # take the Gaussian term is decided by roundoff)
+        # ... anisotropic tensor -> the guard does not fire, (G - M)/eps is live
+        ("wave_v1024_eps1e-12", dict(nx=6, ny=6, vx=(-7.0, 7.0, 32), vy=(-7.0, 7.0, 32),
+                                     faces=("periodic",) * 4, kind="esbgk_2d", nu=-0.5,
+                                     eps=1e-12, ic="wave", gscale=0.0, steps=(1,))),
+        # (one step as well: the macro relaxation at eps = 1e-12 makes the
+        # tensor isotropic to ~1e-13, the guard's knife edge, from step 2 on)
     ]
 
 
@@ -198,6 +213,58 @@ def make_2d(outdir: Path, index):
         print("wrote", name)
 
 
+def make_configs(outdir: Path, index, n=12):
+    """The BASELINE configurations exactly as bench.py builds them
+    (bench.workload_spec + bench.initial_prims: same generators, velocity
+    grids, faces, eps, nu, dt rule), at n x n cells so the reference runs
+    100 steps in seconds.  Stores Q and both heat tensors after 1, 10 and 100
+    steps (G after 100 steps for the wall box and the C5 generator)."""
+    sys.path.insert(0, str(HERE.parents[1]))
+    import bench
+    from micromacro.boundary import EXTRAPOLATE, PERIODIC, BoundarySpec2D, WallSpec
+    from micromacro.gas_state import CollisionModel, conserved_2d, primitives_2d
+    from micromacro.macro2d import heat_flux_tensor_2d
+    from micromacro.mesh import Axis, PhaseMesh, cell_centers
+    from micromacro.runner.loop import State2D, step_2d
+    cases = [("c2", None), ("c3", 1e-3), ("c3", 1e-2), ("c3", 1e-1), ("c4", None), ("c5", None)]
+    for name, eps in cases:
+        spec = bench.workload_spec(name, n=n, eps=eps)
+        lo, hi, nv = spec["vel"]
+        mesh = PhaseMesh(space=(Axis(0.0, spec["Lx"], n), Axis(0.0, spec["Ly"], n)),
+                         velocity=(Axis(lo, hi, nv), Axis(lo, hi, nv)))
+        if spec["faces"] == "periodic":
+            bc = BoundarySpec2D(PERIODIC, PERIODIC, PERIODIC, PERIODIC)
+        elif spec["faces"] == "extrapolate":
+            bc = BoundarySpec2D(EXTRAPOLATE, EXTRAPOLATE, EXTRAPOLATE, EXTRAPOLATE)
+        else:
+            w = WallSpec(temperature=1.0, velocity=0.0)
+            bc = BoundarySpec2D(w, w, w, w)
+        model = CollisionModel(spec["kind"], nu=spec["nu"])
+        rho, u1, u2, T = bench.initial_prims(spec, 0, n, 0, n)
+        Q0 = conserved_2d(rho, u1, u2, T, 0 * T, T)
+        st = State2D(t=0.0, Q=np.array(Q0), G=np.zeros((n, n, nv, nv)))
+        v1 = cell_centers(mesh.velocity[0])
+        v2 = cell_centers(mesh.velocity[1])
+        out = dict(Q0=Q0, dt=spec["dt"])
+        for k in range(1, 101):
+            _, u1n, u2n, _, _, _ = primitives_2d(st.Q)
+            new = step_2d(st, mesh, bc, spec["eps"], model, spec["dt"])
+            if k in (1, 10, 100):
+                out[f"Q{k}"] = new.Q
+                out[f"Hstep{k}"] = np.array(heat_flux_tensor_2d(new.G, u1n, u2n, v1, v2, spec["eps"]))
+                _, a1, a2, _, _, _ = primitives_2d(new.Q)
+                out[f"Hframe{k}"] = np.array(heat_flux_tensor_2d(new.G, a1, a2, v1, v2, spec["eps"]))
+                if k == 100 and name in ("c4", "c5"):
+                    out["G100"] = new.G
+            st = new
+        tag = f"cfg_{name}" + (f"_eps{eps:g}" if eps is not None else "") + f"_n{n}"
+        np.savez_compressed(outdir / f"{tag}.npz", **out)
+        index[tag] = {"config": name, "n": n, "eps": spec["eps"], "dt": spec["dt"],
+                      "faces": spec["faces"], "seed": spec["seed"], "steps": [1, 10, 100],
+                      "generator": "bench.workload_spec / bench.initial_prims"}
+        print("wrote", tag)
+
+
 def make_errors(outdir: Path, index):
     """InvalidStateError cases: the reference's cell and value."""
     from micromacro.boundary import PERIODIC, BoundarySpec2D
@@ -215,6 +282,11 @@ def make_errors(outdir: Path, index):
     q = base.copy(); q[3, 2, 0] = -0.5; q[4, 1, 0] = -1.0; variants["density"] = q
     q = base.copy(); q[2, 4, 4] = 5.0; variants["pressure_spd"] = q   # |T12| > sqrt(T11 T22)
     q = base.copy(); q[1, 3, 3] = 0.005; variants["pressure_t11"] = q
+    # (round 2) several failing cells of different checks: the reference
+    # checks density over the whole field before the tensor, so the density
+    # cell is raised although an SPD failure sits at an earlier cell
+    q = base.copy(); q[0, 1, 4] = 5.0; q[4, 3, 0] = -0.2; q[5, 4, 0] = -0.1
+    variants["density_and_spd"] = q
     for name, Q in variants.items():
         try:
             step_2d(State2D(0.0, Q, np.zeros((6, 5, 6, 6))), mesh, bc, 0.1, model, 1e-3)
@@ -360,6 +432,7 @@ def main():
         index["scipy"] = scipy.__version__
         make_kernels(HERE, index)
         make_2d(HERE, index)
+        make_configs(HERE, index)
         make_1d(HERE, index)
         make_errors(HERE, index)
         make_mms(HERE, index)

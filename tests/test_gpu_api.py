@@ -1,0 +1,134 @@
+"""Behaviour of the drop-in API on the device (round-2 fixes):
+
+* a loop of step_2d calls never synchronises the host with the device
+  (errors stay sticky on the context and surface when the state is read);
+* the solver cache never destroys a context a live state still uses
+  (a sweep over more problems than the cache holds keeps every result);
+* a failing step reports the reference's first offending cell even when
+  several cells of different checks fail, and later steps on the failed
+  state keep reporting that same cell;
+* the multi-rank benchmark path (bench.run_ours_multi) runs end to end with
+  two ranks over gloo (exchanges staged through host memory, so no kernel
+  waits on another rank on this single GPU).
+"""
+
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT, golden_index
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mm():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2509_21832_b200 as mm
+    from paper_2509_21832_b200 import _native
+    _native.load()
+    return mm
+
+
+def test_step_2d_loop_issues_no_host_sync(mm):
+    """100 step_2d calls on C5's generator at 512^2 (~1.4 ms of device time
+    per step) return to the host while the device is still working."""
+    import torch
+    import bench
+    cfg = bench.make_workload("c5", n=512)
+    st = mm.State2D(0.0, cfg["initial"](0, 512, 0, 512), np.zeros((512, 512, 32, 32)))
+    st = mm.step_2d(st, cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"], cfg["dt"])
+    _ = st.Q                                   # warm (solver, graphs, allocator)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(100):
+        st = mm.step_2d(st, cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"], cfg["dt"])
+    host_s = time.perf_counter() - t0
+    done = torch.cuda.Event()
+    done.record()
+    busy = not done.query()
+    torch.cuda.synchronize()
+    dev_t0 = torch.cuda.Event(enable_timing=True)
+    dev_t1 = torch.cuda.Event(enable_timing=True)
+    dev_t0.record()
+    for _ in range(20):
+        st = mm.step_2d(st, cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"], cfg["dt"])
+    dev_t1.record()
+    torch.cuda.synchronize()
+    dev_ms_per_step = dev_t0.elapsed_time(dev_t1) / 20
+    assert busy, f"the host waited for the device: loop took {host_s * 1e3:.1f} ms"
+    assert host_s * 1e3 < 100 * dev_ms_per_step
+    assert np.isfinite(st.Q).all()
+
+
+def test_cache_eviction_keeps_live_states(mm):
+    """More distinct problems than the 4-entry solver cache: every state
+    stays readable and equals a fresh computation."""
+    from paper_2509_21832_b200 import (Axis, BoundarySpec2D, CollisionModel, PERIODIC,
+                                       PhaseMesh, conserved_2d)
+    mesh = PhaseMesh(space=(Axis(0.0, 1.0, 8), Axis(0.0, 1.0, 8)),
+                     velocity=(Axis(-6.0, 6.0, 8), Axis(-6.0, 6.0, 8)))
+    bc = BoundarySpec2D(PERIODIC, PERIODIC, PERIODIC, PERIODIC)
+    x = (np.arange(8) + 0.5) / 8
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    Q = conserved_2d(1.0 + 0.1 * np.sin(2 * np.pi * X), 0.1 + 0 * X, 0 * X, 1.0 + 0 * X,
+                     0 * X, 1.0 + 0 * X)
+    G = np.zeros((8, 8, 8, 8))
+    model = CollisionModel("esbgk_2d", nu=-0.5)
+    eps_list = [0.3, 0.1, 0.03, 0.01, 3e-3, 1e-3, 3e-4]
+    states = [mm.step_2d(mm.State2D(0.0, Q, G), mesh, bc, e, model, 1e-3) for e in eps_list]
+    for e, st in zip(eps_list, states):
+        again = mm.step_2d(mm.State2D(0.0, Q, G), mesh, bc, e, model, 1e-3)
+        assert np.array_equal(st.Q, again.Q)
+        assert np.array_equal(st.G, again.G)
+
+
+def test_error_cell_is_stable_across_later_steps(mm):
+    """density_and_spd: the reference raises the density cell although an
+    SPD failure sits at an earlier cell; stepping the failed state further
+    (no read in between) still reports that cell and value."""
+    from paper_2509_21832_b200 import (Axis, BoundarySpec2D, CollisionModel, PERIODIC,
+                                       PhaseMesh)
+    want = golden_index()["errors"]["density_and_spd"]
+    Q = np.load(GOLDEN / "err_density_and_spd_Q.npy")
+    mesh = PhaseMesh(space=(Axis(0.0, 1.0, 6), Axis(0.0, 1.0, 5)),
+                     velocity=(Axis(-5.0, 5.0, 6), Axis(-5.0, 5.0, 6)))
+    bc = BoundarySpec2D(PERIODIC, PERIODIC, PERIODIC, PERIODIC)
+    model = CollisionModel("esbgk_2d", nu=-0.5)
+    st = mm.State2D(0.0, Q, np.zeros((6, 5, 6, 6)))
+    for _ in range(4):
+        st = mm.step_2d(st, mesh, bc, 0.1, model, 1e-3)
+    with pytest.raises(mm.InvalidStateError) as ei:
+        _ = st.Q
+    assert list(ei.value.cell) == want["cell"]
+    assert ei.value.value == pytest.approx(want["value"], rel=1e-14)
+    # reported once: a fresh valid state on the same problem steps cleanly
+    good = np.load(GOLDEN / "err_density_Q.npy").copy()
+    good[3, 2, 0] = 1.0
+    good[4, 1, 0] = 1.0
+    ok = mm.step_2d(mm.State2D(0.0, good, np.zeros((6, 5, 6, 6))), mesh, bc, 0.1, model, 1e-3)
+    assert np.isfinite(ok.Q).all()
+
+
+def test_multirank_bench_path_over_gloo(mm):
+    """bench.run_ours_multi with 2 ranks (gloo, host-staged exchanges):
+    the decomposed step loop, both exchanges, max-over-ranks timing and
+    the JSON line."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29731", str(ROOT / "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "c2", "--backend", "gloo"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "dd2x1"
+    assert d["gpu_launches"] > 0

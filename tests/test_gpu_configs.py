@@ -1,0 +1,163 @@
+"""GPU parity on the BASELINE configurations exactly as bench.py builds them.
+
+Every case takes its initial state from bench.workload_spec /
+bench.initial_prims -- the generators the benchmark times -- and compares
+the CUDA path (public step_2d / Solver2D.run through the C ABI) with
+
+  * the reference itself: tests/golden/cfg_*_n12.npz, made by running the
+    reference solver on the same generators at 12^2 cells (make_golden.py),
+    after 1, 10 and 100 steps;
+  * the CPU oracle at the benchmark's own sizes: C2 at 256^2 (1 and 100
+    steps), C3 at 512^2 for eps in {1e-3, 1e-2, 1e-1} (1 step), C4's wall
+    box (the bump at 256^2 for 100 steps; 1024^2 for 1 step when host RAM
+    allows), and the C5 generator at 256^2 for 100 steps.
+
+Graded quantities (north star): every conserved moment AND every primitive
+moment (rho, u, T_ab, T, p) within 1e-11 relative L-inf after one step and
+1e-9 after 100 steps, with the SURVEY 8(c) floors (conftest.q_scales,
+conftest.prim_rel_errs); heat tensors within 1e-10 (1e-8 after 100 steps)
+of max(|H_ref|, a 1e-6 eps rho T^1.5 roundoff floor).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import (GOLDEN, golden_cases, golden_index, h_rel_err, prim_rel_errs, q_rel_err,
+                      rel_err)
+
+pytestmark = pytest.mark.gpu
+
+TOL_1 = 1e-11
+TOL_N = 1e-9
+
+
+@pytest.fixture(scope="module")
+def mm():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2509_21832_b200 as mm
+    from paper_2509_21832_b200 import _native
+    _native.load()
+    return mm
+
+
+def _check_moments(Q, Qref, tol, what):
+    e = q_rel_err(Q, Qref)
+    assert e <= tol, (what, "Q", e)
+    pe = prim_rel_errs(Q, Qref)
+    bad = {k: v for k, v in pe.items() if not v <= tol}
+    assert not bad, (what, "primitives", bad)
+
+
+def _workload(name, n, eps=None, seed=0):
+    import bench
+    return bench.make_workload(name, n=n, eps=eps, seed=seed)
+
+
+@pytest.mark.parametrize("name", golden_cases("cfg_"))
+def test_configs_match_reference_goldens(mm, name):
+    """bench.py's generators, 12^2 x 32^2, 100 steps of the public step_2d
+    against the reference's own outputs."""
+    p = golden_index()[name]
+    cfg = _workload(p["config"], p["n"], p["eps"] if p["config"] == "c3" else None, p["seed"])
+    d = np.load(GOLDEN / f"{name}.npz")
+    Q0 = cfg["initial"](0, p["n"], 0, p["n"])
+    assert np.array_equal(Q0, d["Q0"])
+    st = mm.State2D(0.0, Q0, np.zeros((p["n"], p["n"], 32, 32)))
+    for n in range(1, 101):
+        st = mm.step_2d(st, cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"], cfg["dt"])
+        if n in (1, 10, 100):
+            _check_moments(st.Q, d[f"Q{n}"], TOL_1 if n == 1 else TOL_N, (name, n))
+            th = 1e-10 if n == 1 else 1e-8
+            assert h_rel_err(st.H_step.cpu().numpy(), d[f"Hstep{n}"], d[f"Q{n}"],
+                             cfg["eps"]) <= th, (name, n)
+            H = mm.frame_moments(st, cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"])[6:]
+            assert h_rel_err(H, d[f"Hframe{n}"], d[f"Q{n}"], cfg["eps"]) <= th, (name, n)
+    if "G100" in d.files:
+        assert rel_err(st.G, d["G100"]) <= 1e-8
+
+
+def _gpu_steps(mm, cfg, Q0, n_steps):
+    """(Q, G) after n_steps: the first through the public step_2d, the rest
+    as one CUDA-graph replay (Solver2D.run), i.e. both user paths."""
+    import torch
+    nx, ny = cfg["nx"], cfg["ny"]
+    st = mm.State2D(0.0, Q0, np.zeros((nx, ny, 32, 32)))
+    st = mm.step_2d(st, cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"], cfg["dt"])
+    out = {1: (st.Q, st.H_step.cpu().numpy())}
+    if n_steps > 1:
+        solver = mm.get_solver(cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"])
+        Q = torch.from_numpy(st.Q).cuda()
+        G = torch.from_numpy(st.G).cuda()
+        Qf, Gf = solver.run(Q, G, cfg["dt"], n_steps - 1)
+        torch.cuda.synchronize()
+        solver.check()
+        out[n_steps] = (Qf.cpu().numpy(), None)
+        del Gf
+    return out
+
+
+def _oracle_steps(oracle, cfg, Q0, n_steps, keep=(1,)):
+    prob = oracle.Problem2D(cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"])
+    Q, G = Q0, np.zeros((cfg["nx"], cfg["ny"], 32, 32))
+    out = {}
+    for n in range(1, n_steps + 1):
+        Q, G, H = oracle.step_2d_arrays(prob, Q, G, cfg["dt"])
+        if n in keep or n == n_steps:
+            out[n] = (Q, H)
+    return out
+
+
+def _compare(cfg, gpu, cpu, label):
+    for n, (Qo, Ho) in cpu.items():
+        if n not in gpu:
+            continue
+        Qg, Hg = gpu[n]
+        _check_moments(Qg, Qo, TOL_1 if n == 1 else TOL_N, (label, n))
+        if Hg is not None:
+            assert h_rel_err(Hg, Ho, Qo, cfg["eps"]) <= 1e-10, (label, n)
+
+
+def test_c2_full_size_1_and_100_steps_vs_oracle(mm, oracle):
+    """C2 (256^2 x 32^2, the density wave) at its benchmark size."""
+    cfg = _workload("c2", None)
+    Q0 = cfg["initial"](0, 256, 0, 256)
+    _compare(cfg, _gpu_steps(mm, cfg, Q0, 100), _oracle_steps(oracle, cfg, Q0, 100), "c2")
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-2, 1e-1])
+def test_c3_full_size_one_step_vs_oracle(mm, oracle, eps):
+    """C3 (512^2 four-quadrant Riemann, extrapolate faces), every eps."""
+    cfg = _workload("c3", None, eps=eps)
+    Q0 = cfg["initial"](0, 512, 0, 512)
+    _compare(cfg, _gpu_steps(mm, cfg, Q0, 1), _oracle_steps(oracle, cfg, Q0, 1), ("c3", eps))
+
+
+def test_c4_wall_box_bump_100_steps_vs_oracle(mm, oracle):
+    """C4's diffuse-wall box and Gaussian bump at 256^2 for 100 steps."""
+    cfg = _workload("c4", 256)
+    Q0 = cfg["initial"](0, 256, 0, 256)
+    _compare(cfg, _gpu_steps(mm, cfg, Q0, 100), _oracle_steps(oracle, cfg, Q0, 100), "c4@256")
+
+
+def test_c4_full_size_one_step_vs_oracle(mm, oracle):
+    """C4 at its benchmark size (1024^2) for one step, when the host holds
+    the oracle's ~7 copies of G (56 GiB)."""
+    import psutil
+    need = 8 * 1024 * 1024 * 1024 * 8 + (8 << 30)
+    if psutil.virtual_memory().available < need:
+        pytest.skip(f"host RAM: {psutil.virtual_memory().available >> 30} GiB available, "
+                    f"needs {need >> 30}")
+    cfg = _workload("c4", None)
+    Q0 = cfg["initial"](0, 1024, 0, 1024)
+    _compare(cfg, _gpu_steps(mm, cfg, Q0, 1), _oracle_steps(oracle, cfg, Q0, 1), "c4")
+
+
+def test_c5_generator_100_steps_vs_oracle(mm, oracle):
+    """C5's random-Fourier generator (seed 0) at 256^2 for 100 steps."""
+    cfg = _workload("c5", 256)
+    Q0 = cfg["initial"](0, 256, 0, 256)
+    rho = Q0[..., 0]
+    assert rho.min() >= 0.6 - 1e-12
+    _compare(cfg, _gpu_steps(mm, cfg, Q0, 100), _oracle_steps(oracle, cfg, Q0, 100), "c5@256")

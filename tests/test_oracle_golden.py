@@ -11,8 +11,8 @@ import math
 import numpy as np
 import pytest
 
-from conftest import (GOLDEN, golden_cases, golden_index, problem_from_golden, q_rel_err,
-                      rel_err)
+from conftest import (GOLDEN, golden_cases, golden_index, h_rel_err, prim_rel_err,
+                      problem_from_golden, q_rel_err, rel_err)
 
 
 @pytest.mark.parametrize("name", golden_cases("step2d_"))
@@ -26,11 +26,50 @@ def test_oracle_matches_reference_step2d(oracle, name):
         if n in p["steps"]:
             tol = 1e-13 if n == 1 else 1e-11
             assert q_rel_err(Q, d[f"Q{n}"]) <= tol
+            assert prim_rel_err(Q, d[f"Q{n}"]) <= tol
             assert rel_err(G, d[f"G{n}"]) <= 1e-11
             assert rel_err(H, d[f"Hstep{n}"]) <= 1e-11
             Hf = oracle.heat_tensor_2d(G, Q[..., 1] / Q[..., 0], Q[..., 2] / Q[..., 0],
                                        prob.v1, prob.v2, eps)
             assert rel_err(Hf, d[f"Hframe{n}"]) <= 1e-11
+
+
+def config_problem(name, mm=None):
+    """bench.py's workload for a cfg_* golden (the generator the fixture was
+    made with), as this repo's host-side problem objects."""
+    import bench
+    p = golden_index()[name]
+    eps = p["eps"] if p["config"] == "c3" else None
+    return bench.make_workload(p["config"], n=p["n"], eps=eps, seed=p["seed"]), p
+
+
+@pytest.mark.parametrize("name", golden_cases("cfg_"))
+def test_bench_generators_reproduce_golden_inputs(name):
+    """bench.py builds exactly the initial state the reference was run on."""
+    cfg, p = config_problem(name)
+    d = np.load(GOLDEN / f"{name}.npz")
+    assert np.array_equal(cfg["initial"](0, p["n"], 0, p["n"]), d["Q0"])
+    assert cfg["dt"] == float(d["dt"])
+
+
+@pytest.mark.parametrize("name", golden_cases("cfg_"))
+def test_oracle_matches_reference_configs(oracle, name):
+    """The BASELINE configurations as bench.py builds them (12^2 cells,
+    32^2 velocities), 100 steps: moments, primitives and heat tensors."""
+    cfg, p = config_problem(name)
+    d = np.load(GOLDEN / f"{name}.npz")
+    prob = oracle.Problem2D(cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"])
+    Q, G = d["Q0"], np.zeros((p["n"], p["n"], 32, 32))
+    for n in range(1, 101):
+        Qn, G, H = oracle.step_2d_arrays(prob, Q, G, cfg["dt"])
+        if n in (1, 10, 100):
+            tol = 1e-13 if n == 1 else 1e-11
+            assert q_rel_err(Qn, d[f"Q{n}"]) <= tol, n
+            assert prim_rel_err(Qn, d[f"Q{n}"]) <= tol, n
+            assert h_rel_err(H, d[f"Hstep{n}"], d[f"Q{n}"], cfg["eps"]) <= 1e-10, n
+        Q = Qn
+    if "G100" in d.files:
+        assert rel_err(G, d["G100"]) <= 1e-10
 
 
 @pytest.mark.parametrize("name", golden_cases("step1d_"))
@@ -85,7 +124,7 @@ def test_oracle_kernel_contract_matches_reference():
                                         v40[1] - v40[0]), k["project1d"]) <= 1e-12
 
 
-@pytest.mark.parametrize("case", ["density", "pressure_spd", "pressure_t11"])
+@pytest.mark.parametrize("case", ["density", "pressure_spd", "pressure_t11", "density_and_spd"])
 def test_oracle_reports_reference_error_cell(oracle, case):
     from types import SimpleNamespace as NS
     want = golden_index()["errors"][case]
