@@ -130,13 +130,26 @@ def prim_rel_err(Q, Qref):
 
 
 def h_rel_err(H, Href, Qref, eps):
-    """Heat tensor error relative to max(max |Href|, 1e-6 eps rho T^1.5):
+    """Heat tensor error relative to max(max |Href|, 1e-4 eps rho T^1.5):
     the floor keeps roundoff-level heat tensors (e.g. C2's first step, where
     the micro field is pure roundoff) from being graded as signal."""
     p = prims(Qref)
-    floor = 1e-6 * eps * float(np.max(p[0])) * float(np.max(p[6])) ** 1.5
+    floor = 1e-4 * eps * float(np.max(p[0])) * float(np.max(p[6])) ** 1.5
     return float(np.max(np.abs(np.asarray(H) - np.asarray(Href)))) / max(
         float(np.max(np.abs(Href))), floor)
+
+
+def heat_sum_scale(G, eps, v1, v2):
+    """eps dv max_cell sum_n |v|^3 |G_n|: the magnitude of the terms the heat
+    tensor sums.  When they cancel to many digits (eps -> 0 with an
+    anisotropic tensor: G ~ (Gaussian - M) / eps is huge while its heat
+    moment is tiny) a different summation order legitimately differs by
+    roundoff of THIS scale, so 1e-5 of it floors heat-tensor comparisons."""
+    v1 = np.asarray(v1)
+    v2 = np.asarray(v2)
+    vmax = max(float(np.max(np.abs(v1))), float(np.max(np.abs(v2))))
+    dv = (v1[1] - v1[0]) * (v2[1] - v2[0])
+    return eps * dv * vmax ** 3 * float(np.max(np.sum(np.abs(G), axis=(-2, -1))))
 
 
 def rel_err(a, b, floor=1e-300):
