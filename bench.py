@@ -694,6 +694,15 @@ def run_ours(args, rank, world, local_rank):
     step_bytes = bytes_per_step(solver.bx, solver.by, V)
     step_gbs = step_bytes / (ms_step / 1e3) / 1e9
     traffic, traffic_note = micro_traffic(lib, cfg_name)
+    if args.no_e2e:   # A/B timing runs: device numbers only
+        print(json.dumps({"metric": METRIC, "value": value, "ms_per_step": ms_step,
+                          "config": public_config(cfg, world), "clocks": clk,
+                          "roofline": {"frac": achieved / peak, "launch_ms": kms[2],
+                                       "step_frac": step_gbs / peak,
+                                       "kernel_ms": {k: v for k, v in zip(
+                                           ["", "prep", "micro", "", "macro_x", "macro_y", ""],
+                                           kms) if k}}}), flush=True)
+        return
 
     # end to end of a whole run the way a run_2d caller sees it: the host
     # state uploaded once, the config's step count advanced on the device
@@ -885,6 +894,8 @@ def main():
     ap.add_argument("--serial-steps", type=int, default=3,
                     help="reference arm: timed serial step_2d steps on one core")
     ap.add_argument("--no-port", action="store_true", help="reference arm: skip the port line")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="A/B timing: print the device-timed numbers only (no e2e, no CPU arm)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", 0))

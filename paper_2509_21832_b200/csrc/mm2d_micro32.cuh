@@ -31,7 +31,7 @@
 // version of this kernel: bump on every change that alters its code, so
 // committed ncu captures (profiles/micro_traffic.json) stay tied to it
 #ifndef M32_KERNEL_VERSION
-#define M32_KERNEL_VERSION 26
+#define M32_KERNEL_VERSION 27
 #endif
 
 #ifndef MICRO32_MINB
@@ -76,7 +76,8 @@ constexpr int KT = 0;                // K-table [32][KW]
 constexpr int LT = KT + KW * NV;     // L-table [8][32]
 constexpr int GK = LT + 8 * NV;      // Gaussian k-table [32][2] (GA, GD)
 constexpr int GL = GK + 2 * NV;      // Gaussian l-table [32] (GB)
-constexpr int XT = GL + NV;          // Gaussian cross-term table [16][4] per even l + R^8 [16]
+constexpr int XT = GL + NV;          // Gaussian cross-term tables per even l = 2 lp:
+                                     //   (X0, R)[16], (R^2, R^4)[16] as double2, R^8[16]
 constexpr int TAB = XT + 5 * 16;     // 816 doubles per cell
 // K-table pairs (16-byte loads): (w1, h1) (pE1, W1) (cx w1, cx h1) (W1^2, W1^3)
 // (pE1 f0, pE1 f1) (pE1 f2, pE1) -- the target polynomial's W2-power
@@ -89,9 +90,11 @@ enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_F0, K_F1, K_F2, K_PE1B };
 #endif
 // L-table rows: E2, w2, h2, W2, E2 W2, E2 W2^2, f3 E2 W2^3
 enum { L_E2, L_W2N, L_H2, L_W2, L_EW1, L_EW2, L_EW3, L_PAD };
-// cross-term table per even l = 2 lp: X0 = exp(q12 W1_0 W2), R = exp(q12 dv1 W2),
-// R^2, R^4, R^8 (the thread's base node k = kb gets X0 R^kb, its next pairs R^8)
-enum { X_X0, X_R1, X_R2, X_R4, X_R8 = 4 * 16 };   // X_R8: offset of the R^8 row
+// cross-term tables per even l = 2 lp: X0 = exp(q12 W1_0 W2), R = exp(q12 dv1 W2),
+// R^2, R^4, R^8 (the thread's base node k = kb gets X0 R^kb, its next pairs
+// R^8); lp-major with a 16-byte stride, so a quarter-warp's eight lp read
+// 128 contiguous bytes (the previous 32-byte stride took 8 wavefronts)
+enum { X_X0R = 0, X_R24 = 2 * 16, X_R8 = 4 * 16 };
 
 inline size_t smem_bytes() {
     return sizeof(double) * (3 * V + TSLOTS * TAB + 4 * 16 + 16 + 2 * NV);
@@ -224,8 +227,11 @@ __device__ __forceinline__ void reduce12_begin(const double (&v)[12], double* sr
     __syncthreads();
 }
 
+// (phase B: the heat totals go straight to the heat ring from their
+// reducer threads; every thread reads back the 8 projection totals)
 template <int NT_>
-__device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
+__device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred, double* hdst,
+                                             double hfac) {
     constexpr int NS = NT_ >= 128 ? M32_NS : 4;  // segments per value (threads per value)
     constexpr int SEG = NT_ / NS;           // partials per (value, segment)
     constexpr int L2N = SEG / 2;            // double2 loads per segment
@@ -253,11 +259,14 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred) {
         if (NS >= 8) acc += __shfl_xor_sync(0xffffffffu, acc, 4);
         if (NS >= 4) acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         if (NS >= 2) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        if (act && seg == 0) sred[12 * NT_ + vid] = acc;
+        if (act && seg == 0) {
+            if (vid < 8) sred[12 * NT_ + vid] = acc;
+            else if (hdst) hdst[vid - 8] = hfac * acc;
+        }
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 12; q += 2) {
+    for (int q = 0; q < 8; q += 2) {
         const double2 x = lds2(sred + 12 * NT_ + q);
         v[q] = x.x;
         v[q + 1] = x.y;
@@ -320,15 +329,14 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         const int lp = m & 15;
         const double W2e = v2s[2 * lp] - P.u2;
         const double x = fexp(P.gq12 * (m < 16 ? v1s[0] - P.u1 : v1s[1] - v1s[0]) * W2e, etab);
-        double* X = T + XT + 4 * lp;
+        double* X = T + XT;
         if (m < 16) {
-            X[X_X0] = x;
+            X[X_X0R + 2 * lp] = x;
         } else {
             const double r2 = x * x, r4 = r2 * r2;
-            X[X_R1] = x;
-            X[X_R2] = r2;
-            X[X_R4] = r4;
-            T[XT + X_R8 + lp] = r4 * r4;
+            X[X_X0R + 2 * lp + 1] = x;
+            sts2(X + X_R24 + 2 * lp, r2, r4);
+            X[X_R8 + lp] = r4 * r4;
         }
     } else {
         // the exp-free K-table pairs (off warp 0's critical path)
@@ -671,7 +679,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     const bool negy = v2s[lb] < 0.0;
     const double sy = negy ? -a.dt : a.dt;
     const double cy0 = sy * v2s[lb] * a.idy, cy1 = sy * v2s[lb + 1] * a.idy;
-    const int xsel = lp * 4;       // this thread's cross-term table row
+    const int xsel = lp * 2;       // this thread's cross-term table entries
     cp_async_wait_all();
     __syncthreads();
 
@@ -886,8 +894,8 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 for (int p = 0; p < NP_; ++p) Xq[p] = 0.0;
                 if (gauss) {
                     GB = lds2(T + GL + lb);
-                    const double2 x0 = lds2(T + XT + xsel + X_X0);   // X0, R
-                    const double2 r24 = lds2(T + XT + xsel + X_R2);  // R^2, R^4
+                    const double2 x0 = lds2(T + XT + X_X0R + xsel);   // X0, R
+                    const double2 r24 = lds2(T + XT + X_R24 + xsel);  // R^2, R^4
                     const double r8 = T[XT + X_R8 + lp];
                     const double xb = (x0.x * ((kb & 1) ? x0.y : 1.0)) *
                                       (((kb & 2) ? r24.x : 1.0) * ((kb & 4) ? r24.y : 1.0));
@@ -931,9 +939,10 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 }
             }
         }
-        reduce12_end<NT_>(s, sred);
-        if ((ST || (j - 1 >= j0s && j - 1 < j1s)) && tid < 4)
-            a.Hr[4 * ring_index(g, i, j - 1) + tid] = a.hfac * sred[12 * NT_ + 8 + tid];
+        reduce12_end<NT_>(s, sred,
+                          (ST || (j - 1 >= j0s && j - 1 < j1s)) ? a.Hr + 4 * ring_index(g, i, j - 1)
+                                                                : nullptr,
+                          a.hfac);
         if (do_x) {
             ax[0] = s[4]; ax[1] = s[5]; ax[2] = s[6]; ax[3] = s[7];
         }

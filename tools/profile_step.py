@@ -20,8 +20,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--n", type=int, default=None, help="cells per axis (default: the config's)")
     args = ap.parse_args()
-    cfg = bench.make_workload(args.config)
+    cfg = bench.make_workload(args.config, n=args.n)
     s = Solver2D(cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"])
     Q = torch.from_numpy(cfg["initial"](0, cfg["nx"], 0, cfg["ny"])).cuda()
     G = torch.zeros((cfg["nx"], cfg["ny"], 32, 32), dtype=torch.float64, device="cuda")
