@@ -188,13 +188,21 @@ class DistExchange:
 
 class LoopbackExchange:
     """Slot exchange between blocks held by one process: copy every active
-    send slot into the neighbour's opposite receive slot."""
+    send slot into the neighbour's opposite receive slot.
+
+    Ordering is stream-side only (no host synchronisation): a copy runs on
+    the destination device's current stream after an event recorded on the
+    source device's current stream (so after the pack kernel that filled the
+    send buffer), and the source stream waits for the copies out of its
+    buffers before anything it enqueues next (the next pack)."""
 
     def __init__(self, plans, bufs_per_block):
         self.plans = plans
         self.bufs = bufs_per_block
 
     def exchange(self, field):
+        import torch
+        copies = []
         for p in self.plans:
             for s in range(8):
                 peer = p.slots[s]
@@ -203,7 +211,34 @@ class LoopbackExchange:
                 send, _ = self.bufs[p.rank][field][s]
                 _, recv = self.bufs[peer][field][OPPOSITE[s]]
                 if send is not None and recv is not None:
-                    recv.copy_(send, non_blocking=True)
+                    copies.append((send, recv))
+        cross = [(a, b) for a, b in copies if a.device != b.device]
+        if not cross:
+            for send, recv in copies:
+                recv.copy_(send, non_blocking=True)
+            return
+        devs = sorted({t.device.index for c in copies for t in c})
+        ready = {}
+        for d in devs:
+            with torch.cuda.device(d):
+                ready[d] = torch.cuda.Event()
+                ready[d].record()
+        waited = set()
+        for send, recv in copies:
+            a, b = send.device.index, recv.device.index
+            with torch.cuda.device(b):
+                if a != b and (a, b) not in waited:
+                    torch.cuda.current_stream().wait_event(ready[a])
+                    waited.add((a, b))
+                recv.copy_(send, non_blocking=True)
+        done = {}
+        for d in devs:
+            with torch.cuda.device(d):
+                done[d] = torch.cuda.Event()
+                done[d].record()
+        for a, b in waited:
+            with torch.cuda.device(a):
+                torch.cuda.current_stream().wait_event(done[b])
 
     def start(self, field):
         self.exchange(field)
@@ -303,9 +338,7 @@ def step_blocks(blocks, exchange, states, dt):
         with torch.cuda.device(b.solver.device):
             b.pack(FIELD_Q, st[0])
             b.pack(FIELD_G, st[1])
-    _sync_devices(blocks)
     exchange.exchange(FIELD_Q)
-    _sync_devices(blocks)
     hg = exchange.start(FIELD_G)
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
@@ -319,7 +352,6 @@ def step_blocks(blocks, exchange, states, dt):
         with torch.cuda.device(b.solver.device), torch.cuda.stream(b.side):
             b.side.wait_event(b.ev_prep)
             exchange.finish(hg)   # (a started exchange may be finished more than once)
-    _sync_devices(blocks)
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
             with torch.cuda.stream(b.side):
@@ -327,33 +359,53 @@ def step_blocks(blocks, exchange, states, dt):
                 b.ev_side.record()
             torch.cuda.current_stream().wait_event(b.ev_side)
             b.pack(FIELD_H, None)
-    _sync_devices(blocks)
     exchange.exchange(FIELD_H)
-    _sync_devices(blocks)
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
             b.unpack(FIELD_H)
             b.phase(1, st[0], st[1], dt, st[2], st[3], st[4])
 
 
-def _sync_devices(blocks):
-    """Order cross-device copies after the producing kernels (loopback over
-    several GPUs); a no-op cost when every block shares one device."""
-    import torch
-    devs = sorted({b.solver.device.index for b in blocks})
-    if len(devs) > 1:
-        for d in devs:
-            torch.cuda.synchronize(d)
+class CapturedSteps:
+    """The decomposed step of blocks that share one GPU, captured as two
+    CUDA graphs (ping-pong between the (Q, G) and (Q_out, G_out) buffers of
+    every block): a step is one graph launch instead of the ~8 C-ABI calls,
+    halo copies and stream hand-offs per block that step_blocks issues from
+    Python.  Replays are bitwise the eager step_blocks."""
+
+    def __init__(self, blocks, exchange, states, dt):
+        import torch
+        self.graphs = []
+        dev = blocks[0].solver.device
+        views = [states, [[st[2], st[3], st[0], st[1], st[4]] for st in states]]
+        # (capturing records the work without running it: the states are
+        # untouched until the first replay)
+        with torch.cuda.device(dev):
+            for v in views:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    step_blocks(blocks, exchange, v, dt)
+                self.graphs.append(g)
+        self.parity = 0
+
+    def step(self):
+        self.graphs[self.parity].replay()
+        self.parity ^= 1
 
 
 def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), track_from=None,
-                    devices=None):
+                    devices=None, graph=True):
     """Advance n_steps with a rows x cols block grid spread over the visible
     GPUs (blocks round-robin over ``devices``); returns
     (Q, G, steady_max, seconds) like the reference (parallel.py:404-473).
     steady_max is the largest per-step max-norm change of Q over steps
     >= track_from (NaN if untracked); seconds is the wall time of the
-    stepping loop (device-synchronised, excluding setup and gathers)."""
+    stepping loop (device-synchronised, excluding setup and gathers).
+
+    When every block sits on one GPU and no steady-state tracking is asked
+    for, the loop replays CUDA graphs of the decomposed step (``graph``);
+    otherwise it is issued eagerly, ordered across GPUs by stream events
+    only (no host synchronisation inside the loop)."""
     import torch
     nx, ny = mesh.space[0].n, mesh.space[1].n
     plans = make_plans(nx, ny, grid, bc)
@@ -372,17 +424,30 @@ def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), trac
         states.append([Q, G, torch.empty_like(Q), torch.empty_like(G), H])
     exchange = LoopbackExchange(plans, [b.bufs for b in blocks])
     steady = 0.0
+    one_device = len({b.solver.device.index for b in blocks}) == 1
+    captured = None
+    if graph and one_device and track_from is None and n_steps >= 2:
+        captured = CapturedSteps(blocks, exchange, states, dt)
     for d in devices:
         torch.cuda.synchronize(d)
     t0 = time.perf_counter()
-    for n in range(n_steps):
-        step_blocks(blocks, exchange, states, dt)
-        if track_from is not None and n >= track_from:
+    if captured is not None:
+        with torch.cuda.device(blocks[0].solver.device):
+            for n in range(n_steps):
+                captured.step()
+        if n_steps % 2:
             for st in states:
-                steady = max(steady, float((st[2] - st[0]).abs().max()))
-        for st in states:
-            st[0], st[2] = st[2], st[0]
-            st[1], st[3] = st[3], st[1]
+                st[0], st[2] = st[2], st[0]
+                st[1], st[3] = st[3], st[1]
+    else:
+        for n in range(n_steps):
+            step_blocks(blocks, exchange, states, dt)
+            if track_from is not None and n >= track_from:
+                for st in states:
+                    steady = max(steady, float((st[2] - st[0]).abs().max()))
+            for st in states:
+                st[0], st[2] = st[2], st[0]
+                st[1], st[3] = st[3], st[1]
     for d in devices:
         torch.cuda.synchronize(d)
     seconds = time.perf_counter() - t0
@@ -399,4 +464,4 @@ def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), trac
 
 
 __all__ = ["HaloPlan", "make_plans", "DistExchange", "LoopbackExchange", "BlockStepper",
-           "halo_buffers", "step_blocks", "run_parallel_2d", "SLOTS", "OPPOSITE"]
+           "halo_buffers", "step_blocks", "CapturedSteps", "run_parallel_2d", "SLOTS", "OPPOSITE"]

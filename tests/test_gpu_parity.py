@@ -273,6 +273,26 @@ def test_block_grid_equals_serial_bitwise(mm, grid, faces, nv):
     assert np.array_equal(Gp, st.G)
 
 
+@pytest.mark.parametrize("nsteps", [1, 5])
+def test_block_grid_graph_replay_equals_eager(mm, nsteps):
+    """run_parallel_2d's CUDA-graph replay of the decomposed step (blocks on
+    one GPU) is bitwise its eager issue and the serial step, for an odd step
+    count too (the ping-pong parity)."""
+    from paper_2509_21832_b200 import PERIODIC, WallSpec
+    from paper_2509_21832_b200.parallel import run_parallel_2d
+    w = WallSpec(1.0)
+    mesh, bc, model, Q0, G0 = _parallel_problem(12, 12, 32, (PERIODIC, PERIODIC, w, w), 5)
+    dt = 0.3 * (1.0 / 12) / 5.0
+    Qg, Gg, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, nsteps, grid=(2, 3))
+    Qe, Ge, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, nsteps, grid=(2, 3),
+                                   graph=False)
+    st = mm.State2D(0.0, Q0, G0)
+    for _ in range(nsteps):
+        st = mm.step_2d(st, mesh, bc, 0.08, model, dt)
+    assert np.array_equal(Qg, Qe) and np.array_equal(Gg, Ge)
+    assert np.array_equal(Qg, st.Q) and np.array_equal(Gg, st.G)
+
+
 def test_block_grid_steady_tracking(mm):
     from paper_2509_21832_b200 import PERIODIC
     from paper_2509_21832_b200.parallel import run_parallel_2d
