@@ -55,6 +55,31 @@ __host__ __device__ inline unsigned long long err_key(unsigned step, unsigned st
 }
 constexpr unsigned long long kNoError = ~0ull;
 
+// Debug build (make EXTRA=-DMM2D_DEBUG_CHECKS=1 OUT=../libmm2d_dbg.so):
+// device-side bounds checks on the shared-memory, tensor-memory and global
+// indices the kernels compute; a failed check prints the site and traps.
+// This stands in for compute-sanitizer, which is closed on the GPU pool
+// (profiles/r02_compute_sanitizer_closed.log).  Release builds compile the
+// checks away.
+#ifndef MM2D_DEBUG_CHECKS
+#define MM2D_DEBUG_CHECKS 0
+#endif
+#if MM2D_DEBUG_CHECKS
+#include <cstdio>
+#define MM2D_CHECK(cond)                                                                   \
+    do {                                                                                   \
+        if (!(cond)) {                                                                     \
+            printf("MM2D_CHECK failed: %s at %s:%d (block %d,%d thread %d)\n", #cond,      \
+                   __FILE__, __LINE__, (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x); \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define MM2D_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 // Error words of a context (8 x u64): [0] E, the merged key of every
 // completed kernel; [1..4] isotropy maxima; [5] R_prep, [6] R_mx, [7] R_my,
 // the keys raised by k_prep, k_macro_x and k_macro_y.  A kernel raises into

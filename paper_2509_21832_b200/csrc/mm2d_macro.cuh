@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(MX_TJ * (MX_TI + 2)) k_macro_x(MacroArgs a) {
             atomicMin(a.err + EW_MX, err_key(a.step, bs == 1 ? ES_XS_RHO : ES_XS_SPD, gcell));
         }
     }
+    MM2D_CHECK(i >= -1 && i <= g.bx && j >= -1 && j <= g.by);
     double* o = a.Qx + 6 * ring_index(g, i, j);
 #pragma unroll
     for (int m = 0; m < 6; ++m) {
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(128) k_macro_y(MacroArgs a) {
         const double Fp = (0.0 + L[m]) + Ru[m];
         q3[m] = qc[m] - a.ry * (Fp - Fm);
     }
+    MM2D_CHECK(i >= 0 && i < g.bx && j >= -1 && j <= g.by);
     const double* hc = a.Hr + 4 * ring_index(g, i, j);
     double hd[4], hu[4];
     load_ring_h(g, a.Hr, i, j - 1, hd);

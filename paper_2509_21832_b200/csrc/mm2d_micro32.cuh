@@ -552,6 +552,13 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     double* v2s = v1s + NV;
     double* etab = v2s + NV + 2;                    // [64] 2^(i/64)
     const size_t V_ = V;
+#if MM2D_DEBUG_CHECKS
+    {
+        unsigned dyn;
+        asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        MM2D_CHECK((size_t)(etab + 64 + 2 - smem) * sizeof(double) <= dyn);
+    }
+#endif
 
     const int i = blockIdx.x;
     const int j0s = a.nband ? a.band_j0[blockIdx.y] : blockIdx.y * a.ly;
@@ -636,6 +643,22 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             if (!hl) hl = a.zero;
             if (!hr) hr = a.zero;
         }
+#if MM2D_DEBUG_CHECKS
+        {
+            auto inbuf = [&](const double* p, int half) {
+                const double* e = p + (half ? V / 2 : V);
+                const size_t nG = (size_t)g.bx * g.by * V_;
+                return (p >= a.G && e <= a.G + nG) || (p >= a.zero && e <= a.zero + V_) ||
+                       (a.hxlo && p >= a.hxlo && e <= a.hxlo + (size_t)g.by * V_) ||
+                       (a.hxhi && p >= a.hxhi && e <= a.hxhi + (size_t)g.by * V_) ||
+                       (a.hylo && p >= a.hylo && e <= a.hylo + (size_t)(g.bx + 2) * V_) ||
+                       (a.hyhi && p >= a.hyhi && e <= a.hyhi + (size_t)(g.bx + 2) * V_);
+            };
+            MM2D_CHECK(inbuf(own, 0));
+            MM2D_CHECK(inbuf(hr, 1));
+            MM2D_CHECK(inbuf(hl + V / 2, 1));
+        }
+#endif
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_expect_tx(mbar, 2 * V * sizeof(double));
         bulk_g2s(stg, own, V * sizeof(double), mbar);
@@ -700,6 +723,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     // rotating slot pointers: ring rows (j-1, j, j+1); table rows
     // (j, j+1, j+2, j+3, j-1)
     unsigned R0 = tq, R1 = tq + 16, R2 = tq + 32;   // TMEM ring rows (j-1, j, j+1)
+    MM2D_CHECK(off_(NP_ - 1) + 2 <= V && koff_(NP_ - 1) + KW <= LT && xsel + 2 <= 2 * 16);
     double* T0 = tabs;
     double* T1 = tabs + SLOT;
     double* T2 = tabs + 2 * SLOT;
@@ -757,6 +781,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             const double bE0 = fma(w2.x, a3, h2.x * a4) * E2.x;
             const double bE1 = fma(w2.y, a3, h2.y * a4) * E2.y;
+            MM2D_CHECK(R2 >= tq && R2 + 16 <= tq + TM_COLS && R1 >= tq && R0 >= tq);
             tm_ld8(R2, gst);
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
@@ -960,6 +985,8 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
             const double bE0 = fma(w2.x, a3, h2.x * a4) * E2.x;
             const double bE1 = fma(w2.y, a3, h2.y * a4) * E2.y;
+            MM2D_CHECK(j >= 0 && j < g.by && j >= j0s && j < j1s);
+            MM2D_CHECK(T0 >= tabs && T0 + SLOT <= tabs + TSLOTS * SLOT);
             double* out = out_b + (size_t)j * V_;
             double A0x, A0y, A1x, A1y, A2x, A2y, A3x, A3y;
 #pragma unroll

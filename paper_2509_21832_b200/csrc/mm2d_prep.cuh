@@ -308,7 +308,10 @@ __global__ void k_prep(PrepArgs a) {
             }
         }
         prep_cell(a, t, i, j, [&](int s, int d, int k) { return w[s][d][k]; },
-                  [&](const CellPar& P) { reinterpret_cast<CellPar*>(a.P)[t] = P; });
+                  [&](const CellPar& P) {
+                      MM2D_CHECK(t >= 0 && t < n);
+                      reinterpret_cast<CellPar*>(a.P)[t] = P;
+                  });
     }
 }
 
@@ -368,6 +371,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_prep_tiled(PrepArgs a) {
         // the warp's tile row is nrow contiguous CellPars: write them as
         // 512-byte coalesced runs of double2
         if (ri < g.bx + 2) {
+            MM2D_CHECK(rj0 + nrow <= g.by + 2 && nrow > 0);
             double* dst = reinterpret_cast<double*>(a.P) + ((size_t)ri * (g.by + 2) + rj0) * 32;
             const double* wst = stage + (threadIdx.x - lj) * 32;
             for (int f = 2 * lj; f < nrow * 32; f += 64) {
