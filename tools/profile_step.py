@@ -21,13 +21,20 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--n", type=int, default=None, help="cells per axis (default: the config's)")
+    ap.add_argument("--run", action="store_true",
+                    help="ping-pong through Solver2D.run (two state buffers, no allocations "
+                         "per step: the C5 state is 32 GiB per copy)")
     args = ap.parse_args()
     cfg = bench.make_workload(args.config, n=args.n)
     s = Solver2D(cfg["mesh"], cfg["bc"], cfg["eps"], cfg["model"])
     Q = torch.from_numpy(cfg["initial"](0, cfg["nx"], 0, cfg["ny"])).cuda()
     G = torch.zeros((cfg["nx"], cfg["ny"], 32, 32), dtype=torch.float64, device="cuda")
-    for _ in range(args.steps):
-        Q, G, H = s.step(Q, G, cfg["dt"])
+    if args.run:
+        Qb, Gb = s.empty_state()
+        Q, G = s.run(Q, G, cfg["dt"], args.steps, Q_b=Qb, G_b=Gb)
+    else:
+        for _ in range(args.steps):
+            Q, G, H = s.step(Q, G, cfg["dt"])
     torch.cuda.synchronize()
     s.check()
     print("ok", float(Q[..., 0].sum()))
