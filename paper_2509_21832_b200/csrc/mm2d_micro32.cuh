@@ -216,7 +216,16 @@ __device__ __forceinline__ double tsum(const double (&c)[N]) {
     else return c[0];
 }
 
+#ifndef M32_TMEM_RED
+#define M32_TMEM_RED 0   // 1: warp-level row reduction through tensor memory (measured); 0: shared memory
+#endif
+#if M32_TMEM_RED
+// per-warp totals [4][12] + the 8 projection totals, sharing the space with
+// the specular exchange (NP doubles per thread, two rounds)
+template <int NT_> constexpr int red_size() { return NT_ * 4; }   // doubles
+#else
 template <int NT_> constexpr int red_size() { return 12 * NT_ + 16; }   // doubles
+#endif
 
 // phase A: store partials, barrier.  phase B + totals: reduce12_end.  Work
 // that touches neither the partials nor the totals may sit in between.
@@ -497,7 +506,96 @@ __device__ __forceinline__ void tm_ld8(unsigned addr, double (&v)[8]) {
 __device__ __forceinline__ void tm_wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
+#if M32_TMEM_RED
+// Row reduction of the 12 per-thread sums (y | x | heat) without shared-
+// memory partials: the L1TEX pipe that shared memory and shuffles share is
+// the kernel's binding resource, the tensor-memory port is not.
+// Phase A, per warp: each thread stores its 12 sums in its own TMEM lane
+// (columns tred .. tred + 23); 16x256b loads hand thread t the sums
+// (t % 4) + 4 r (r = 0..2) of lanes t / 4, t / 4 + 8, t / 4 + 16 and
+// t / 4 + 24, which it adds; three shuffle levels over the lane bits 2-4
+// finish the warp total, and lanes 0-3 store the warp's 12 totals; barrier.
+// Phase B (reduce12_end_tm): 12 threads add the four warps' totals, the
+// heat totals go straight to the heat ring; barrier; every thread reads the
+// 8 projection totals.  Fixed order throughout, so results stay bitwise
+// reproducible.
+__device__ __forceinline__ void tm_ld16x256_x2(unsigned addr, double (&v)[4]) {
+    asm volatile(
+        "{\n .reg .b32 a<8>;\n"
+        " tcgen05.ld.sync.aligned.16x256b.x2.b32 {a0, a1, a2, a3, a4, a5, a6, a7}, [%4];\n"
+        " mov.b64 %0, {a0, a1};\n mov.b64 %1, {a2, a3};\n mov.b64 %2, {a4, a5};\n"
+        " mov.b64 %3, {a6, a7};\n}\n"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+        : "r"(addr)
+        : "memory");
+}
+__device__ __forceinline__ void tm_ld16x256_x1(unsigned addr, double (&v)[2]) {
+    asm volatile(
+        "{\n .reg .b32 a<4>;\n"
+        " tcgen05.ld.sync.aligned.16x256b.x1.b32 {a0, a1, a2, a3}, [%2];\n"
+        " mov.b64 %0, {a0, a1};\n mov.b64 %1, {a2, a3};\n}\n"
+        : "=d"(v[0]), "=d"(v[1])
+        : "r"(addr)
+        : "memory");
+}
+
+__device__ __forceinline__ void reduce12_begin_tm(const double (&v)[12], double* sred,
+                                                  unsigned tred) {
+    tm_st_n<8>(tred, v);
+    tm_st_n<4>(tred + 16, v + 8);
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncwarp();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // lanes 0-15 then 16-31 of the warp's quadrant; per load: [lane t/4, r]
+    // [lane t/4 + 8, r] for r = 0, 1 (x2) and r = 2 (x1)
+    double a01[4], a2[2], b01[4], b2[2];
+    tm_ld16x256_x2(tred, a01);
+    tm_ld16x256_x1(tred + 16, a2);
+    tm_ld16x256_x2(tred + (16u << 16), b01);
+    tm_ld16x256_x1(tred + (16u << 16) + 16, b2);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    double q[3] = {(a01[0] + a01[1]) + (b01[0] + b01[1]), (a01[2] + a01[3]) + (b01[2] + b01[3]),
+                   (a2[0] + a2[1]) + (b2[0] + b2[1])};
+#pragma unroll
+    for (int m = 4; m <= 16; m <<= 1)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) q[r] += __shfl_xor_sync(0xffffffffu, q[r], m);
+    const int lane = threadIdx.x & 31;
+    if (lane < 4) {
+        double* w = sred + 12 * (threadIdx.x >> 5) + lane;
+        w[0] = q[0];
+        w[4] = q[1];
+        w[8] = q[2];
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void reduce12_end_tm(double (&v)[12], double* sred, double* hdst,
+                                                double hfac) {
+    // warp 1 (a reducer-free warp's table work is on warp 0) adds the warp totals
+    const int r = (int)threadIdx.x - 32;
+    if (r >= 0 && r < 12) {
+        const double t = (sred[r] + sred[12 + r]) + (sred[24 + r] + sred[36 + r]);
+        if (r < 8) sred[48 + r] = t;
+        else if (hdst) hdst[r - 8] = hfac * t;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+        const double2 x = lds2(sred + 48 + q);
+        v[q] = x.x;
+        v[q + 1] = x.y;
+    }
+}
+#endif
+
+#if M32_TMEM_RED
+constexpr int TM_COLS = 128;         // G* ring (3 rows x 16 columns) + the row reduction (24)
+constexpr int TM_RED = 64;           // first reduction column
+#else
 constexpr int TM_COLS = 64;          // 3 rows x 16 columns, rounded to a power of two
+#endif
 
 template <int NP_>
 inline size_t smem_bytes_v3() {
@@ -745,6 +843,27 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     // this thread's pair (lb, lb+1) is pair 30 - lb of the thread with the
     // same k base in the partner warp (tid ^ 0x27), swapped.  Exchanged
     // through the (idle) reduction partials; CTA-uniform call sites only.
+#if M32_TMEM_RED
+    // (half a row per round: the reduction area holds NP doubles per thread)
+    static_assert(red_size<NT_>() >= NP_ * NT_, "mirror exchange needs NP doubles per thread");
+    auto mirror_l = [&](double (&v)[2 * NP_]) {
+        double* xch = sred;
+        const int pt = tid ^ 0x27;
+#pragma unroll
+        for (int h = 0; h < 2 * NP_; h += NP_) {
+#pragma unroll
+            for (int q = 0; q < NP_; q += 2) sts2(xch + NP_ * tid + q, v[h + q], v[h + q + 1]);
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < NP_; q += 2) {
+                const double2 x = lds2(xch + NP_ * pt + q);
+                v[h + q] = x.y;
+                v[h + q + 1] = x.x;
+            }
+            __syncthreads();
+        }
+    };
+#else
     auto mirror_l = [&](double (&v)[2 * NP_]) {
         double* xch = sred;
 #pragma unroll
@@ -759,6 +878,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         }
         __syncthreads();
     };
+#endif
 
     auto body = [&](int j, auto steady) {
         constexpr bool ST = decltype(steady)::value;
@@ -886,7 +1006,11 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         // 4. the row's block reduction; the CellPar staged one iteration
         //    ago (row j+4) lands before it
         cp_async_wait_prev();
+#if M32_TMEM_RED
+        reduce12_begin_tm(s, sred, tq + TM_RED);
+#else
         reduce12_begin<NT_>(s, sred);
+#endif
         // every thread is past this row's x-stage reads: refill the staging
         if (ST || computes(rx + 1)) prefetch(rx + 1, steady);
         // tables for row j+3, built while the reduction's second phase runs:
@@ -964,7 +1088,11 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 }
             }
         }
+#if M32_TMEM_RED
+        reduce12_end_tm(s, sred,
+#else
         reduce12_end<NT_>(s, sred,
+#endif
                           (ST || (j - 1 >= j0s && j - 1 < j1s)) ? a.Hr + 4 * ring_index(g, i, j - 1)
                                                                 : nullptr,
                           a.hfac);
