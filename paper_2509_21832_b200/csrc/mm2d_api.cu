@@ -532,6 +532,8 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     ma.dt = dt; ma.eps = c.eps; ma.inveps = 1.0 / c.eps;
     ma.idx = 1.0 / g.dx; ma.idy = 1.0 / g.dy;
     ma.dv = pa.dv; ma.hfac = c.eps * pa.dv;
+    ma.ikx = dt != 0.0 ? g.dx / dt : 0.0; ma.iky = dt != 0.0 ? g.dy / dt : 0.0;
+    ma.ikx2 = ma.ikx * ma.ikx; ma.ryx = (g.dy / g.dx) * (g.dy / g.dx);
     ma.wall_ghat = ctx->d_wallg;
     ma.zero = ctx->d_zero;
     ma.part = part;

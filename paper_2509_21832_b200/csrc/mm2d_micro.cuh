@@ -54,6 +54,9 @@ struct MicroArgs {
     int part;                 // 0 all CTAs; 1 only CTAs that read no received G halo
                               // (run while the halo exchange is in flight); 2 only the others
     double dt, eps, inveps, idx, idy, dv, hfac;  // hfac = eps * dv
+    // k_micro32's raw-moment projection sums: dx/dt, dy/dt, (dx/dt)^2, (dy/dx)^2
+    // (the scales between its node coordinates dt |v| / dx and the velocities)
+    double ikx, iky, ikx2, ryx;
 };
 
 // Does the CTA owning columns [i0, i1) and rows [j0, j1) read a received G

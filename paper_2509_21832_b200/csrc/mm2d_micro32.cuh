@@ -31,7 +31,21 @@
 // version of this kernel: bump on every change that alters its code, so
 // committed ncu captures (profiles/micro_traffic.json) stay tied to it
 #ifndef M32_KERNEL_VERSION
-#define M32_KERNEL_VERSION 27
+#define M32_KERNEL_VERSION 28
+#endif
+
+// Projection sums in raw velocity moments (v28).  1: each thread weights its
+// upwind differences with its own, cell-independent node coordinates (the
+// sign-folded upwind coefficients it already holds in registers), the row
+// reduction adds raw moments (1, v1, v2, |v|^2), and the reducer warp of each
+// stage converts the four totals once per cell into the coefficients of the
+// projection polynomial c0 + c1 v1 + c2 v2 + c3 |v|^2 (raw_to_coef), which
+// every thread evaluates at its nodes again from registers.  The K-table
+// loses (w1, h1), (cx w1, cx h1) and the L-table w2, h2: 24 of a thread's 52
+// shared-memory table loads per row.  0: the v27 form (normalised basis
+// w1, w2, b4 from the tables).
+#ifndef M32_RAW
+#define M32_RAW 1
 #endif
 
 #ifndef MICRO32_MINB
@@ -67,14 +81,16 @@ constexpr int TSLOTS = 4;            // table slots (rows j..j+3; the slot rebui
 #define M32_W1POW_TABLE 1
 #endif
 #endif
-#if M32_W1POW_TABLE
-constexpr int KW = 12;               // K-table entries per k
+#if M32_RAW
+constexpr int KW = M32_W1POW_TABLE ? 8 : 6;     // K-table entries per k
+constexpr int LR = 6;                           // L-table rows
 #else
-constexpr int KW = 10;               // K-table entries per k
+constexpr int KW = M32_W1POW_TABLE ? 12 : 10;   // K-table entries per k
+constexpr int LR = 8;
 #endif
 constexpr int KT = 0;                // K-table [32][KW]
-constexpr int LT = KT + KW * NV;     // L-table [8][32]
-constexpr int GK = LT + 8 * NV;      // Gaussian k-table [32][2] (GA, GD)
+constexpr int LT = KT + KW * NV;     // L-table [LR][32]
+constexpr int GK = LT + LR * NV;     // Gaussian k-table [32][2] (GA, GD)
 constexpr int GL = GK + 2 * NV;      // Gaussian l-table [32] (GB)
 constexpr int XT = GL + NV;          // Gaussian cross-term tables per even l = 2 lp:
                                      //   (X0, R)[16], (R^2, R^4)[16] as double2, R^8[16]
@@ -83,6 +99,15 @@ constexpr int TAB = XT + 5 * 16;     // 816 doubles per cell
 // (pE1 f0, pE1 f1) (pE1 f2, pE1) -- the target polynomial's W2-power
 // coefficients pre-multiplied by the Maxwellian's k factor, the x-sum weights
 // by the upwind coefficient
+#if M32_RAW
+#if M32_W1POW_TABLE
+enum { K_PE1, K_W1, K_W12, K_W13, K_F0, K_F1, K_F2, K_PE1B };
+#else
+enum { K_PE1, K_W1, K_F0, K_F1, K_F2, K_PE1B };
+#endif
+// L-table rows: E2, W2, E2 W2, E2 W2^2, f3 E2 W2^3
+enum { L_E2, L_W2, L_EW1, L_EW2, L_EW3, L_PAD };
+#else
 #if M32_W1POW_TABLE
 enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_W12, K_W13, K_F0, K_F1, K_F2, K_PE1B };
 #else
@@ -90,6 +115,7 @@ enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_F0, K_F1, K_F2, K_PE1B };
 #endif
 // L-table rows: E2, w2, h2, W2, E2 W2, E2 W2^2, f3 E2 W2^3
 enum { L_E2, L_W2N, L_H2, L_W2, L_EW1, L_EW2, L_EW3, L_PAD };
+#endif
 // cross-term tables per even l = 2 lp: X0 = exp(q12 W1_0 W2), R = exp(q12 dv1 W2),
 // R^2, R^4, R^8 (the thread's base node k = kb gets X0 R^kb, its next pairs
 // R^8); lp-major with a 16-byte stride, so a quarter-warp's eight lp read
@@ -144,7 +170,7 @@ __device__ __forceinline__ void reduce16(double (&v)[16], double* sred) {
 
 // Row header stored in each table slot (doubles): per-cell scalars the node
 // loops need, so they come from shared memory instead of global loads.
-enum { H_SCALE, H_WG, H_MTW, H_MEW, H_GQ12, H_WH, H_N = 8 };
+enum { H_SCALE, H_WG, H_MTW, H_MEW, H_GQ12, H_WH, H_U1, H_U2, H_IST, H_INVT, H_N = 12 };
 constexpr int HD = TAB;              // header offset inside a slot
 constexpr int SLOT = TAB + H_N;      // doubles per table slot
 
@@ -238,9 +264,40 @@ __device__ __forceinline__ void reduce12_begin(const double (&v)[12], double* sr
 
 // (phase B: the heat totals go straight to the heat ring from their
 // reducer threads; every thread reads back the 8 projection totals)
+#if M32_RAW
+// Totals of a stage's raw moments N0 = sum Y, N1 = sum (s xi) Y, N2 = sum (s' eta) Y,
+// N3 = sum (xi^2 + ryx eta^2) Y, in the threads' node coordinates xi = dt |v1| / dx,
+// eta = dt |v2| / dy  ->  the coefficients of the projection polynomial
+// q = C0 + C1 (s xi) + C2 (s' eta) + C3 (xi^2 + ryx eta^2), scaled by sc, with
+// Pi[Y] = q M (_core.pyx:171-199: the normalised sums A1..A4 of the basis
+// 1, w1, w2, b4 = (w1^2 + w2^2)/2 - 1, expanded about the cell's u and T).
+__device__ __forceinline__ void raw_to_coef(const MicroArgs& a, const double* hdr, double sc,
+                                            double N0, double N1, double N2, double N3,
+                                            double (&C)[4]) {
+    const double2 u = lds2(hdr + H_U1);
+    const double2 tt = lds2(hdr + H_IST);          // 1/sqrt(T), 1/T
+    const double isT = tt.x, invT = tt.y;
+    const double m1 = N1 * a.ikx, m2 = N2 * a.iky, m3 = N3 * a.ikx2;
+    const double uu = fma(u.x, u.x, u.y * u.y);
+    const double A2 = isT * fma(-u.x, N0, m1);
+    const double A3 = isT * fma(-u.y, N0, m2);
+    const double A4 = fma(0.5 * invT, fma(uu, N0, fma(-2.0, fma(u.x, m1, u.y * m2), m3)), -N0);
+    const double a1 = N0 * sc, a2 = A2 * sc, a3 = A3 * sc, a4 = A4 * sc;
+    const double c3 = 0.5 * a4 * invT;
+    const double c1 = fma(a2, isT, -2.0 * c3 * u.x);
+    const double c2 = fma(a3, isT, -2.0 * c3 * u.y);
+    const double c0 = fma(c3, uu, fma(-isT, fma(a2, u.x, a3 * u.y), a1 - a4));
+    C[0] = c0;
+    C[1] = c1 * a.ikx;
+    C[2] = c2 * a.iky;
+    C[3] = c3 * a.ikx2;
+}
+#endif
+
 template <int NT_>
 __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred, double* hdst,
-                                             double hfac) {
+                                             double hfac, const MicroArgs& a, const double* Ty,
+                                             const double* Tx) {
     constexpr int NS = NT_ >= 128 ? M32_NS : 4;  // segments per value (threads per value)
     constexpr int SEG = NT_ / NS;           // partials per (value, segment)
     constexpr int L2N = SEG / 2;            // double2 loads per segment
@@ -268,10 +325,29 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred, doub
         if (NS >= 8) acc += __shfl_xor_sync(0xffffffffu, acc, 4);
         if (NS >= 4) acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         if (NS >= 2) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+#if M32_RAW
+        // warp 0 of the reducers holds the y totals (vid 0-3, eight lanes each),
+        // warp 1 the x totals: gather the four, convert once per cell
+        static_assert(NT_ < 128 || M32_NS == 8, "raw-moment conversion assumes 8 lanes per value");
+        if (tid < 64) {
+            const double N0 = __shfl_sync(0xffffffffu, acc, 0), N1 = __shfl_sync(0xffffffffu, acc, 8);
+            const double N2 = __shfl_sync(0xffffffffu, acc, 16), N3 = __shfl_sync(0xffffffffu, acc, 24);
+            const bool isy = tid < 32;
+            const double* hdr = (isy ? Ty : Tx) + HD;
+            const double2 sw = lds2(hdr + H_SCALE);        // scale, wg
+            double Cf[4];
+            raw_to_coef(a, hdr, isy ? sw.x * sw.y : sw.x, N0, N1, N2, N3, Cf);
+            if ((tid & 31) == 0) {
+                sts2(sred + 12 * NT_ + (isy ? 0 : 4), Cf[0], Cf[1]);
+                sts2(sred + 12 * NT_ + (isy ? 2 : 6), Cf[2], Cf[3]);
+            }
+        } else if (act && seg == 0 && hdst) hdst[vid - 8] = hfac * acc;
+#else
         if (act && seg == 0) {
             if (vid < 8) sred[12 * NT_ + vid] = acc;
             else if (hdst) hdst[vid - 8] = hfac * acc;
         }
+#endif
     }
     __syncthreads();
 #pragma unroll
@@ -317,16 +393,20 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
             sts2(T + HD + H_SCALE, P.scale, P.wg);
             sts2(T + HD + H_MTW, mtw, a.inveps * P.wh);
             sts2(T + HD + H_GQ12, P.gq12, P.wh);
+            sts2(T + HD + H_U1, P.u1, P.u2);
+            sts2(T + HD + H_IST, P.isT, P.invT);
         }
     } else if (t < 64) {
         const double W2 = v2s[m] - P.u2;
         const double W2s = W2 * W2;
-        const double w2 = W2 * P.isT;
         const double E2 = fexp(-W2s * P.inv2T, etab);
         double* L = T + LT + m;
         L[L_E2 * NV] = E2;
+#if !M32_RAW
+        const double w2 = W2 * P.isT;
         L[L_W2N * NV] = w2;
         L[L_H2 * NV] = 0.5 * w2 * w2;
+#endif
         L[L_W2 * NV] = W2;
         L[L_EW1 * NV] = E2 * W2;
         L[L_EW2 * NV] = E2 * W2s;
@@ -351,13 +431,15 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         // the exp-free K-table pairs (off warp 0's critical path)
         const double W1 = v1s[m] - P.u1;
         const double W1s = W1 * W1;
+        double* K = T + KT + KW * m;
+#if !M32_RAW
         const double w1 = W1 * P.isT;
         const double h1 = 0.5 * w1 * w1 - 1.0;
         // the x-stage upwind coefficient (sign folded: v1 < 0 exactly for k < 16)
         const double cxm = (m < NV / 2 ? -a.dt : a.dt) * v1s[m] * a.idx;
-        double* K = T + KT + KW * m;
         sts2(K + K_W1N, w1, h1);
         sts2(K + K_XW, cxm * w1, cxm * h1);
+#endif
 #if M32_W1POW_TABLE
         sts2(K + K_W12, W1s, W1s * W1);
 #endif
@@ -590,6 +672,9 @@ __device__ __forceinline__ void reduce12_end_tm(double (&v)[12], double* sred, d
 }
 #endif
 
+#if M32_TMEM_RED && M32_RAW
+#error "M32_TMEM_RED is only implemented for the v27 (M32_RAW=0) reduction"
+#endif
 #if M32_TMEM_RED
 constexpr int TM_COLS = 128;         // G* ring (3 rows x 16 columns) + the row reduction (24)
 constexpr int TM_RED = 64;           // first reduction column
@@ -800,6 +885,9 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     const bool negy = v2s[lb] < 0.0;
     const double sy = negy ? -a.dt : a.dt;
     const double cy0 = sy * v2s[lb] * a.idy, cy1 = sy * v2s[lb + 1] * a.idy;
+    // x with the sign of the thread's v2 (one XOR on the high word)
+    const int sbit = negy ? (int)0x80000000 : 0;
+    auto sflip = [&](double x) { return __hiloint2double(__double2hiint(x) ^ sbit, __double2loint(x)); };
     const int xsel = lp * 2;       // this thread's cross-term table entries
     cp_async_wait_all();
     __syncthreads();
@@ -894,20 +982,33 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         tm_wait_st();
         if (ST || computes(rc)) {
             const double* T = T1;
+            const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
+#if M32_RAW
+            // projection polynomial of the x-stage totals at the thread's nodes,
+            // split as (C0 + C1 s xi + C3 xi^2) + eta (C2 s' + C3 ryx eta)
+            const double c2s = sflip(ax[2]), c3y = ax[3] * a.ryx;
+            const double bE0 = cy0 * fma(c3y, cy0, c2s) * E2.x;
+            const double bE1 = cy1 * fma(c3y, cy1, c2s) * E2.y;
+#else
             const double sc = T[HD + H_SCALE];
             const double a1 = ax[0] * sc, a2 = ax[1] * sc, a3 = ax[2] * sc, a4 = ax[3] * sc;
-            const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
             const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
             const double bE0 = fma(w2.x, a3, h2.x * a4) * E2.x;
             const double bE1 = fma(w2.y, a3, h2.y * a4) * E2.y;
+#endif
             MM2D_CHECK(R2 >= tq && R2 + 16 <= tq + TM_COLS && R1 >= tq && R0 >= tq);
             tm_ld8(R2, gst);
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
-                const double2 wh = lds2(T + koff_(p) + K_W1N);   // w1, h1
                 const double pe = T[koff_(p) + K_PE1];
+#if M32_RAW
+                const double alp =
+                    fma(cx[p], fma(ax[3], cx[p], p < NP_ / 2 ? -ax[1] : ax[1]), ax[0]) * pe;
+#else
+                const double2 wh = lds2(T + koff_(p) + K_W1N);   // w1, h1
                 const double alp = fma(wh.x, a2, fma(wh.y, a4, a1)) * pe;
+#endif
                 gst[2 * p] = fma(alp, E2.x, fma(bE0, pe, gst[2 * p]));
                 gst[2 * p + 1] = fma(alp, E2.y, fma(bE1, pe, gst[2 * p + 1]));
             }
@@ -948,8 +1049,10 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             double c[2 * NP_];
             tm_ld8(R1, c);
             tm_ld8(negy ? R2 : R0, gst);
+#if !M32_RAW
             const double2 w2 = lds2(T0 + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T0 + LT + L_H2 * NV + lb);
+#endif
             double D0, D1, S1, S3;
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
@@ -957,26 +1060,44 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 ty[2 * p] = fma(-cy0, d0, c[2 * p]);
                 ty[2 * p + 1] = fma(-cy1, d1, c[2 * p + 1]);
                 const double e = fma(cy0, d0, cy1 * d1);
+#if M32_RAW
+                // raw moments of Y in the thread's coordinates: s xi, xi^2
+                const double t = cx[p] * e;
+                if (p == 0) {
+                    D0 = d0; D1 = d1; S1 = -t; S3 = cx[p] * t;
+                } else {
+                    D0 += d0; D1 += d1; S1 = p < NP_ / 2 ? S1 - t : S1 + t; S3 = fma(cx[p], t, S3);
+                }
+#else
                 const double2 wh = lds2(T0 + koff_(p) + K_W1N);   // w1, h1
                 if (p == 0) {
                     D0 = d0; D1 = d1; S1 = wh.x * e; S3 = wh.y * e;
                 } else {
                     D0 += d0; D1 += d1; S1 = fma(wh.x, e, S1); S3 = fma(wh.y, e, S3);
                 }
+#endif
             }
             const double Y0 = cy0 * D0, Y1 = cy1 * D1;
             s[0] = Y0 + Y1;
             s[1] = S1;
+#if M32_RAW
+            const double z0 = cy0 * Y0, z1 = cy1 * Y1;
+            s[2] = sflip(z0 + z1);
+            s[3] = fma(a.ryx, fma(cy0, z0, cy1 * z1), S3);
+#else
             s[2] = fma(w2.x, Y0, w2.y * Y1);
             s[3] = S3 + fma(h2.x, Y0, h2.y * Y1);
+#endif
         }
         // 3. x-stage of row j+2 into the slot of row j-1: G - dt Z_x = G - cx d
         const bool do_x = ST || computes(rx);
         if (do_x) {
             mbar_wait(mbar, (nload - 1) & 1);   // this row's bulk loads (issued one iteration ago)
+#if !M32_RAW
             const double* T = T2;
             const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
+#endif
             double xs[2 * NP_];
             double Y0, Y1, S1, S3;
 #pragma unroll
@@ -988,6 +1109,15 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 xs[2 * p] = fma(-cx[p], d0, c.x);
                 xs[2 * p + 1] = fma(-cx[p], d1, c.y);
                 const double e = d0 + d1;
+#if M32_RAW
+                const double t = cx[p] * (cx[p] * e);              // xi (y0 + y1)
+                if (p == 0) {
+                    Y0 = cx[p] * d0; Y1 = cx[p] * d1; S1 = -t; S3 = cx[p] * t;
+                } else {
+                    Y0 = fma(cx[p], d0, Y0); Y1 = fma(cx[p], d1, Y1);
+                    S1 = p < NP_ / 2 ? S1 - t : S1 + t; S3 = fma(cx[p], t, S3);
+                }
+#else
                 const double2 xw = lds2(T + koff_(p) + K_XW);      // cx w1, cx h1
                 if (p == 0) {
                     Y0 = cx[p] * d0; Y1 = cx[p] * d1; S1 = xw.x * e; S3 = xw.y * e;
@@ -995,12 +1125,19 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                     Y0 = fma(cx[p], d0, Y0); Y1 = fma(cx[p], d1, Y1);
                     S1 = fma(xw.x, e, S1); S3 = fma(xw.y, e, S3);
                 }
+#endif
             }
             tm_st8(R0, xs);
             s[4] = Y0 + Y1;
             s[5] = S1;
+#if M32_RAW
+            const double z0 = cy0 * Y0, z1 = cy1 * Y1;
+            s[6] = sflip(z0 + z1);
+            s[7] = fma(a.ryx, fma(cy0, z0, cy1 * z1), S3);
+#else
             s[6] = fma(w2.x, Y0, w2.y * Y1);
             s[7] = S3 + fma(h2.x, Y0, h2.y * Y1);
+#endif
         }
         s[8] = hs[0]; s[9] = hs[1]; s[10] = hs[2]; s[11] = hs[3];
         // 4. the row's block reduction; the CellPar staged one iteration
@@ -1095,7 +1232,11 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
 #endif
                           (ST || (j - 1 >= j0s && j - 1 < j1s)) ? a.Hr + 4 * ring_index(g, i, j - 1)
                                                                 : nullptr,
-                          a.hfac);
+                          a.hfac
+#if !M32_TMEM_RED
+                          , a, T0, T2
+#endif
+                          );
         if (do_x) {
             ax[0] = s[4]; ax[1] = s[5]; ax[2] = s[6]; ax[3] = s[7];
         }
@@ -1105,14 +1246,21 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             // G^{n+1} = acc + wg Zhat_y, Zhat_y = (a1 + w1 a2 + h1 a4 + w2 a3 + h2 a4) M
             // split as (al pE1) E2 + pE1 (b E2) with wg folded into the a's
             const double* T = T0;
+            const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
+            const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
+#if M32_RAW
+            // (the y totals arrive as polynomial coefficients, scale and wg folded in)
+            const double c2s = sflip(s[2]), c3y = s[3] * a.ryx;
+            const double bE0 = cy0 * fma(c3y, cy0, c2s) * E2.x;
+            const double bE1 = cy1 * fma(c3y, cy1, c2s) * E2.y;
+#else
             const double sc = T[HD + H_SCALE] * T[HD + H_WG];
             const double a1 = s[0] * sc, a2 = s[1] * sc, a3 = s[2] * sc, a4 = s[3] * sc;
-            const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
             const double2 w2 = lds2(T + LT + L_W2N * NV + lb);
             const double2 h2 = lds2(T + LT + L_H2 * NV + lb);
-            const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
             const double bE0 = fma(w2.x, a3, h2.x * a4) * E2.x;
             const double bE1 = fma(w2.y, a3, h2.y * a4) * E2.y;
+#endif
             MM2D_CHECK(j >= 0 && j < g.by && j >= j0s && j < j1s);
             MM2D_CHECK(T0 >= tabs && T0 + SLOT <= tabs + TSLOTS * SLOT);
             double* out = out_b + (size_t)j * V_;
@@ -1120,7 +1268,6 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
                 const double* K = T + koff_(p);
-                const double2 wh = lds2(K + K_W1N);     // w1, h1
                 const double2 pw = lds2(K + K_PE1);     // pE1, W1
 #if M32_W1POW_TABLE
                 const double2 w3 = lds2(K + K_W12);     // W1^2, W1^3
@@ -1129,7 +1276,13 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 w3.x = pw.y * pw.y;
                 w3.y = w3.x * pw.y;
 #endif
+#if M32_RAW
+                const double alp =
+                    fma(cx[p], fma(s[3], cx[p], p < NP_ / 2 ? -s[1] : s[1]), s[0]) * pw.x;
+#else
+                const double2 wh = lds2(K + K_W1N);     // w1, h1
                 const double alp = fma(wh.x, a2, fma(wh.y, a4, a1)) * pw.x;
+#endif
                 const double o0 = fma(alp, E2.x, fma(bE0, pw.x, acc[2 * p]));
                 const double o1 = fma(alp, E2.y, fma(bE1, pw.x, acc[2 * p + 1]));
                 *reinterpret_cast<double2*>(out + off_(p)) = make_double2(o0, o1);
