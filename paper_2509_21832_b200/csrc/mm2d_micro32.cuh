@@ -253,6 +253,16 @@ template <int NT_> constexpr int red_size() { return NT_ * 4; }   // doubles
 template <int NT_> constexpr int red_size() { return 12 * NT_ + 16; }   // doubles
 #endif
 
+// The totals' hand-over (v28): 1: the reducer threads arrive on an mbarrier once
+// their totals are written and every thread waits for that phase, so warp 0
+// (which builds the heaviest table in the same window) is not part of the
+// hand-over and the row has ONE CTA-wide barrier; 0: a second __syncthreads.
+#ifndef M32_MBAR_B
+#define M32_MBAR_B 0
+#endif
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity);
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar);
+
 // phase A: store partials, barrier.  phase B + totals: reduce12_end.  Work
 // that touches neither the partials nor the totals may sit in between.
 template <int NT_>
@@ -297,7 +307,8 @@ __device__ __forceinline__ void raw_to_coef(const MicroArgs& a, const double* hd
 template <int NT_>
 __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred, double* hdst,
                                              double hfac, const MicroArgs& a, const double* Ty,
-                                             const double* Tx) {
+                                             const double* Tx, unsigned long long* mbarB,
+                                             unsigned parityB) {
     constexpr int NS = NT_ >= 128 ? M32_NS : 4;  // segments per value (threads per value)
     constexpr int SEG = NT_ / NS;           // partials per (value, segment)
     constexpr int L2N = SEG / 2;            // double2 loads per segment
@@ -348,8 +359,16 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred, doub
             else if (hdst) hdst[vid - 8] = hfac * acc;
         }
 #endif
+#if M32_MBAR_B
+        mbar_arrive(mbarB);
+#endif
     }
+#if M32_MBAR_B
+    // (also orders the next row's partial stores after the reducers' loads)
+    mbar_wait(mbarB, parityB);
+#else
     __syncthreads();
+#endif
 #pragma unroll
     for (int q = 0; q < 8; q += 2) {
         const double2 x = lds2(sred + 12 * NT_ + q);
@@ -479,6 +498,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
     asm volatile(
@@ -808,9 +830,11 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(v2s + NV);
     if (tid == 0) {
         mbar_init(mbar, 1);
+        mbar_init(mbar + 1, (12 * M32_NS + 31) & ~31);   // the totals: one arrival per thread of the reducer warps
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     unsigned nload = 0;            // bulk loads issued (mbarrier phase = parity)
+    const int jfirst = j0s - (M32_SHORT_FILL ? 3 : 4);   // first row-loop iteration (phase 0 of the totals' mbarrier)
     auto prefetch = [&](int r, auto steady) {
         if (tid != 0) { ++nload; return; }
         const double *own, *hl, *hr;
@@ -1234,7 +1258,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                                                                 : nullptr,
                           a.hfac
 #if !M32_TMEM_RED
-                          , a, T0, T2
+                          , a, T0, T2, mbar + 1, (unsigned)(j - jfirst) & 1
 #endif
                           );
         if (do_x) {
