@@ -31,7 +31,7 @@
 // version of this kernel: bump on every change that alters its code, so
 // committed ncu captures (profiles/micro_traffic.json) stay tied to it
 #ifndef M32_KERNEL_VERSION
-#define M32_KERNEL_VERSION 28
+#define M32_KERNEL_VERSION 29
 #endif
 
 // Projection sums in raw velocity moments (v28).  1: each thread weights its
@@ -379,9 +379,10 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred, doub
 
 // build the per-cell tables from the shared copy P of the cell's CellPar.
 // Warp 0 (which does not reduce) the K-table's Maxwellian factor and the
-// target coefficients it scales, warp 1 the L-table, warp 2 the Gaussian GA
-// and the cross-term table, warp 3 the exp-free K-table pairs and the
-// Gaussian GB and GD: the six exps per cell spread 1 / 1 / 2 / 2.  The closed-form target polynomial is
+// target coefficients it scales, warp 1 the L-table, warp 2 the Gaussian
+// cross-term table, warp 3 the exp-free K-table pairs and the Gaussian GA, GB
+// and GD: the six exps per cell spread 1 / 1 / 1 / 3 (warps 1 and 2 also carry
+// the longest reductions, with the totals' conversion).  The closed-form target polynomial is
 // stored pre-scaled by mtw = -wh/tau with the Gaussian's -M wh/eps folded
 // into U.  As a polynomial in W2 the bracket is f0(k) + f1(k) W2 + f2(k) W2^2
 // + f3 W2^3 (f3 cell-constant), so with the Maxwellian's factors folded in the
@@ -431,8 +432,9 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         L[L_EW2 * NV] = E2 * W2s;
         L[L_EW3 * NV] = (mtw * (P.gT2 * P.invT * P.inv2T)) * (E2 * (W2s * W2));
     } else if (gauss && t < 96) {
-        const double W1 = v1s[m] - P.u1;
-        T[GK + 2 * m] = P.gpref * a.inveps * P.wh * fexp(P.gq11 * (W1 * W1), etab);   // GA'
+        // (GA, the Gaussian's k factor, is built by warp 3: this warp also reduces and
+        // converts the x sums, and the row time follows the busiest warp -- moving
+        // that one exp evened the roles out: C5 -1.0 %, C2 -1.6 %)
         // lanes 0-15: X0 at l = 2m; lanes 16-31: R and its powers at l = 2(m-16)
         const int lp = m & 15;
         const double W2e = v2s[2 * lp] - P.u2;
@@ -464,6 +466,7 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
 #endif
         if (gauss) {
             const double W2 = v2s[m] - P.u2;
+            T[GK + 2 * m] = P.gpref * a.inveps * P.wh * fexp(P.gq11 * W1s, etab);    // GA'
             T[GL + m] = fexp(P.gq22 * (W2 * W2), etab);                              // GB
             T[GK + 2 * m + 1] = fexp(P.gq12 * W1 * (v2s[1] - v2s[0]), etab);         // GD
         }
