@@ -183,6 +183,24 @@ int mm2d_halo_info(mm2d_ctx *ctx, int which, int slot, double **d_send,
 int mm2d_halo_pack(mm2d_ctx *ctx, int which, const double *d_src, void *stream);
 int mm2d_halo_unpack(mm2d_ctx *ctx, int which, void *stream);
 
+/* Peer form of the G halo (no reference counterpart: the reference's workers
+ * copy their strips through shared memory, parallel.py:153-182).  d_nbG[s] is
+ * the base of the CURRENT G^n array (bx, by, nv1, nv2) of the neighbour block
+ * in slot s (NULL for an inactive slot), dereferenceable from this context's
+ * device: a block on the same GPU, a peer GPU with access enabled
+ * (mm2d_enable_peer_access, NVLink / NVSwitch), or a CUDA-IPC mapping of
+ * another process's array.  The micro kernels of the following steps then read
+ * every ghost cell in place from those arrays -- the perimeter CTAs' bulk
+ * copies fetch the halo rows straight from the neighbour's HBM -- so field 0
+ * needs no pack, transfer or receive buffer.  Every block of a decomposition
+ * has this block's shape (make_plans).  The caller orders the steps: a
+ * neighbour's G^n must be complete, and this block's G^{n+1} buffer must no
+ * longer be read by a neighbour, when the step is enqueued (the Q ring
+ * exchange that precedes every step gives both).  Pass NULL to return to the
+ * packed form.  Call again whenever the neighbours' arrays change (ping-pong). */
+int mm2d_halo_peer(mm2d_ctx *ctx, const double *const *d_nbG);
+int mm2d_enable_peer_access(int device, int peer_device);
+
 /* ---- the ten kernel-contract functions (_kernels plugin API) ----
  * device pointers, reference layouts; `ext` arrays carry one ghost layer on
  * the differenced axis. */

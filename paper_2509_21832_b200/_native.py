@@ -98,6 +98,8 @@ SIGNATURES = {
                                  C.POINTER(C.c_longlong)]),
     "mm2d_halo_pack": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "mm2d_halo_unpack": (C.c_int, [_vp, C.c_int, _vp]),
+    "mm2d_halo_peer": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "mm2d_enable_peer_access": (C.c_int, [C.c_int, C.c_int]),
     "mm2d_k_maxwellian_field_2d": (C.c_int, [C.c_int] * 4 + [_vp] * 7 + [_vp]),
     "mm2d_k_project_field_2d": (C.c_int, [C.c_int] * 4 + [_vp] * 8 + [C.c_double, _vp, _vp]),
     "mm2d_k_transport_stage_2d": (C.c_int, [C.c_int] * 4 + [_vp] * 8 +

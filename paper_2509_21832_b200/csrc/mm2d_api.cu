@@ -79,6 +79,9 @@ struct mm2d_ctx {
     // halo staging (multi-rank): [field G/Q/H][slot]
     bool halo_ready = false;
     int halo_cells[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // peer form of the G halos (mm2d_halo_peer): the neighbours' current G arrays
+    const double* peerG[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool peer = false;
     double* hsend[3][8] = {};
     double* hrecv[3][8] = {};
     int sms = 148;                 // multiprocessors of the context's device
@@ -525,6 +528,24 @@ static int enqueue_step(mm2d_ctx* ctx, const double* Q, const double* G, double 
     memset(&ma, 0, sizeof(ma));
     ma.g = g; ma.G = G; ma.Gout = Gout;
     ma.hxlo = ctx->d_gh[0]; ma.hxhi = ctx->d_gh[1]; ma.hylo = ctx->d_gh[2]; ma.hyhi = ctx->d_gh[3];
+    ma.hys = (size_t)g.V;
+    if (ctx->peer) {
+        // the neighbours' G arrays in place (every block of a decomposition
+        // has this block's shape): slot s of mm2d_halo_* order
+        const size_t Vz = (size_t)g.V, col = (size_t)g.by * Vz;
+        const double* const* nb = ctx->peerG;
+        ma.hpeer = 1;
+        ma.hys = col;
+        ma.hxlo = nb[0] ? nb[0] + (size_t)(g.bx - 1) * col : nullptr;       // its last column
+        ma.hxhi = nb[1];                                                     // its first column
+        ma.hylo = nb[2] ? nb[2] + (size_t)(g.by - 1) * Vz - col : nullptr;   // its top row
+        ma.hyhi = nb[3] ? nb[3] - col : nullptr;                             // its bottom row
+        ma.hc[0] = nb[4] ? nb[4] + (size_t)(g.bx - 1) * col + (size_t)(g.by - 1) * Vz : nullptr;
+        ma.hc[1] = nb[5] ? nb[5] + (size_t)(g.by - 1) * Vz : nullptr;
+        ma.hc[2] = nb[6] ? nb[6] + (size_t)(g.bx - 1) * col : nullptr;
+        ma.hc[3] = nb[7];
+        for (int s8 = 0; s8 < 8; ++s8) ma.hnb[s8] = nb[s8];
+    }
     ma.P = ctx->d_P; ma.Hr = ctx->d_Hr; ma.v1 = ctx->d_v1; ma.v2 = ctx->d_v2;
     ma.err = ctx->d_err; ma.iso = ctx->d_err + 1;
     ma.src_coeffs = sc; ma.src_shapes = ss; ma.nsrc = nsrc;
@@ -1071,6 +1092,38 @@ static HaloDesc halo_desc(mm2d_ctx* ctx, int which, bool send) {
     }
     d.width = field_width(ctx->g, which);
     return d;
+}
+
+extern "C" int mm2d_halo_peer(mm2d_ctx* ctx, const double* const* d_nbG) {
+    if (!ctx) return MM2D_ERR_CONFIG;
+    if (!d_nbG) {
+        ctx->peer = false;
+        return MM2D_OK;
+    }
+    const Geometry& g = ctx->g;
+    for (int s = 0; s < 8; ++s) {
+        ctx->peerG[s] = d_nbG[s];
+        if (slot_active(g, s) && !d_nbG[s]) return fail_cfg(ctx, "mm2d_halo_peer: active slot without a neighbour array");
+    }
+    ctx->peer = true;
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_enable_peer_access(int device, int peer_device) {
+    if (device == peer_device) return MM2D_OK;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, device, peer_device) != cudaSuccess || !can)
+        return MM2D_ERR_CONFIG;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    cudaSetDevice(cur);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return MM2D_OK;
+    }
+    return e == cudaSuccess ? MM2D_OK : MM2D_ERR_INTERNAL;
 }
 
 extern "C" int mm2d_halo_pack(mm2d_ctx* ctx, int which, const double* d_src, void* stream) {

@@ -32,10 +32,16 @@ struct MicroArgs {
     Geometry g;
     const double* G;          // (bx, by, V) G^n
     double* Gout;             // (bx, by, V) G^{n+1}
-    const double* hxlo;       // received halos (HALO faces only)
-    const double* hxhi;       //   x: by cells, y: bx + 2 cells (corners at 0, bx+1)
-    const double* hylo;
-    const double* hyhi;
+    const double* hxlo;       // G halos (HALO faces only).  Packed (received) form:
+    const double* hxhi;       //   x: by cells, y: bx + 2 cells (corners at 0, bx+1), hys = V.
+    const double* hylo;       // Peer form (mm2d_halo_peer): the pointers address the
+    const double* hyhi;       //   neighbour blocks' own G arrays, read in place over
+    size_t hys;               //   NVLink / peer memory: x faces are the neighbour's edge
+    const double* hc[4];      //   column (contiguous), y-face cell i sits at hy + (i + 1) hys
+    int hpeer;                //   with hys = by V, and the four corner cells come from the
+                              //   diagonal neighbours (hc: bottom-left, bottom-right,
+                              //   top-left, top-right)
+    const double* hnb[8];     // peer form: the neighbours' G bases (debug bounds checks)
     const CellPar* P;         // ring
     double* Hr;               // ring, AoS [ring][4]
     const double* v1;         // velocity centres
@@ -92,14 +98,16 @@ __device__ __forceinline__ const double* gn_cell(const MicroArgs& a, int i, int 
         const int m = i < 0 ? g.xlo : g.xhi;
         if (m == GM_ZERO) return nullptr;
         if (m == GM_HALO) {
-            if (yhalo) return (r < 0 ? a.hylo : a.hyhi) + (size_t)(i < 0 ? 0 : g.bx + 1) * V;
+            if (yhalo)
+                return a.hpeer ? a.hc[(r < 0 ? 0 : 2) + (i < 0 ? 0 : 1)]
+                               : (r < 0 ? a.hylo : a.hyhi) + (size_t)(i < 0 ? 0 : g.bx + 1) * V;
             return (i < 0 ? a.hxlo : a.hxhi) + (size_t)rr * V;
         }
         if (m == GM_WRAP) ii = (i + g.bx) % g.bx;
         else ii = i < 0 ? 0 : g.bx - 1;
         if (m == GM_MIRROR && mir) *mir = true;
     }
-    if (yhalo) return (r < 0 ? a.hylo : a.hyhi) + (size_t)(ii + 1) * V;
+    if (yhalo) return (r < 0 ? a.hylo : a.hyhi) + (size_t)(ii + 1) * a.hys;
     return a.G + ((size_t)ii * g.by + rr) * V;
 }
 

@@ -858,6 +858,11 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             auto inbuf = [&](const double* p, int half) {
                 const double* e = p + (half ? V / 2 : V);
                 const size_t nG = (size_t)g.bx * g.by * V_;
+                if (a.hpeer) {
+                    for (int s8 = 0; s8 < 8; ++s8)
+                        if (a.hnb[s8] && p >= a.hnb[s8] && e <= a.hnb[s8] + nG) return true;
+                    return (p >= a.G && e <= a.G + nG) || (p >= a.zero && e <= a.zero + V_);
+                }
                 return (p >= a.G && e <= a.G + nG) || (p >= a.zero && e <= a.zero + V_) ||
                        (a.hxlo && p >= a.hxlo && e <= a.hxlo + (size_t)g.by * V_) ||
                        (a.hxhi && p >= a.hxhi && e <= a.hxhi + (size_t)g.by * V_) ||

@@ -313,6 +313,19 @@ class BlockStepper:
         s = self.solver
         s._rc(s.lib.mm2d_halo_unpack(s.ctx, field, self._stream()))
 
+    def set_peers(self, neigh_G):
+        """Peer form of the G halo (mm2d_halo_peer): ``neigh_G[s]`` is the
+        current G tensor (or raw device pointer) of the neighbour in slot s,
+        None for an inactive slot; ``None`` returns to the packed form."""
+        s = self.solver
+        if neigh_G is None:
+            s._rc(s.lib.mm2d_halo_peer(s.ctx, None))
+            return
+        ptrs = (C.c_void_p * 8)(*[None if t is None else
+                                  (int(t) if isinstance(t, int) else t.data_ptr())
+                                  for t in neigh_G])
+        s._rc(s.lib.mm2d_halo_peer(s.ctx, ptrs))
+
     def phase(self, ph, Q, G, dt, Qout, Gout, H):
         s = self.solver
         from .solver import _ptr
@@ -321,9 +334,46 @@ class BlockStepper:
         s._rc(rc)
 
 
-def step_blocks(blocks, exchange, states, dt):
+def peer_views(blocks, states):
+    """Per block, the current G tensors of its eight slot neighbours (all
+    blocks held by this process, indexed by rank)."""
+    return [[None if nb is None else states[nb][1] for nb in b.plan.slots] for b in blocks]
+
+
+def _step_blocks_peer(blocks, exchange, states, dt, peers):
+    """The decomposed step with the G halo in peer form: no G pack, transfer
+    or receive buffer.  Each block's micro kernel (one launch, phase 0) reads
+    its ghost cells in place from the neighbours' G^n arrays -- on another
+    GPU through peer memory (NVLink), the perimeter CTAs' bulk copies
+    fetching the halo rows while the interior CTAs compute.  The Q ring
+    exchange that opens the step orders it against the neighbours: their
+    sends follow their previous step on their streams, so once the ring has
+    arrived their G^n is complete and their reads of this block's G^{n-1}
+    buffer (which this step overwrites) are over."""
+    import torch
+    for b, st, nb in zip(blocks, states, peers):
+        with torch.cuda.device(b.solver.device):
+            b.set_peers(nb)
+            b.pack(FIELD_Q, st[0])
+    exchange.exchange(FIELD_Q)
+    for b, st in zip(blocks, states):
+        with torch.cuda.device(b.solver.device):
+            b.unpack(FIELD_Q)
+            b.phase(0, st[0], st[1], dt, st[2], st[3], st[4])
+            b.pack(FIELD_H, None)
+    exchange.exchange(FIELD_H)
+    for b, st in zip(blocks, states):
+        with torch.cuda.device(b.solver.device):
+            b.unpack(FIELD_H)
+            b.phase(1, st[0], st[1], dt, st[2], st[3], st[4])
+
+
+def step_blocks(blocks, exchange, states, dt, peers=None):
     """One decomposed step for every block held by this process.
     ``states[b] = (Q, G, Qout, Gout, H)`` device tensors of block b.
+    ``peers`` (peer_views, or IPC mappings for one process per GPU) selects
+    the peer form of the G halo (_step_blocks_peer); without it G travels
+    packed:
 
     The G ring exchange (V doubles per perimeter cell, the bulk of the
     traffic) overlaps the interior cells' micro update: the Q ring (6
@@ -334,6 +384,8 @@ def step_blocks(blocks, exchange, states, dt):
     they run concurrently with the interior CTAs instead of after them.
     Phases 4 + 5 + 3 are bitwise the unsplit phase 0."""
     import torch
+    if peers is not None:
+        return _step_blocks_peer(blocks, exchange, states, dt, peers)
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
             b.pack(FIELD_Q, st[0])
@@ -373,7 +425,7 @@ class CapturedSteps:
     halo copies and stream hand-offs per block that step_blocks issues from
     Python.  Replays are bitwise the eager step_blocks."""
 
-    def __init__(self, blocks, exchange, states, dt):
+    def __init__(self, blocks, exchange, states, dt, peer=False):
         import torch
         self.graphs = []
         dev = blocks[0].solver.device
@@ -384,7 +436,8 @@ class CapturedSteps:
             for v in views:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
-                    step_blocks(blocks, exchange, v, dt)
+                    step_blocks(blocks, exchange, v, dt,
+                                peers=peer_views(blocks, v) if peer else None)
                 self.graphs.append(g)
         self.parity = 0
 
@@ -393,8 +446,24 @@ class CapturedSteps:
         self.parity ^= 1
 
 
+def enable_peer_access(blocks):
+    """Peer access between the GPUs of neighbouring blocks (NVLink /
+    NVSwitch); False if some pair cannot be mapped (the packed exchange is
+    used then)."""
+    ok = True
+    lib = blocks[0].solver.lib
+    for b in blocks:
+        for nb in b.plan.slots:
+            if nb is None:
+                continue
+            a, c = b.solver.device.index, blocks[nb].solver.device.index
+            if a != c and lib.mm2d_enable_peer_access(a, c) != 0:
+                ok = False
+    return ok
+
+
 def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), track_from=None,
-                    devices=None, graph=True):
+                    devices=None, graph=True, halo="peer"):
     """Advance n_steps with a rows x cols block grid spread over the visible
     GPUs (blocks round-robin over ``devices``); returns
     (Q, G, steady_max, seconds) like the reference (parallel.py:404-473).
@@ -405,7 +474,12 @@ def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), trac
     When every block sits on one GPU and no steady-state tracking is asked
     for, the loop replays CUDA graphs of the decomposed step (``graph``);
     otherwise it is issued eagerly, ordered across GPUs by stream events
-    only (no host synchronisation inside the loop)."""
+    only (no host synchronisation inside the loop).
+
+    ``halo``: "peer" (default) reads the G ghost cells in place from the
+    neighbour blocks' arrays (peer memory across GPUs; falls back to "packed"
+    when a pair of GPUs has no peer access); "packed" packs, copies and
+    receives the G ring, overlapped with the interior micro CTAs."""
     import torch
     nx, ny = mesh.space[0].n, mesh.space[1].n
     plans = make_plans(nx, ny, grid, bc)
@@ -423,11 +497,12 @@ def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), trac
         H = torch.empty((4,) + p.shape, dtype=torch.float64, device=dev)
         states.append([Q, G, torch.empty_like(Q), torch.empty_like(G), H])
     exchange = LoopbackExchange(plans, [b.bufs for b in blocks])
+    peer = halo == "peer" and enable_peer_access(blocks)
     steady = 0.0
     one_device = len({b.solver.device.index for b in blocks}) == 1
     captured = None
     if graph and one_device and track_from is None and n_steps >= 2:
-        captured = CapturedSteps(blocks, exchange, states, dt)
+        captured = CapturedSteps(blocks, exchange, states, dt, peer=peer)
     for d in devices:
         torch.cuda.synchronize(d)
     t0 = time.perf_counter()
@@ -441,7 +516,8 @@ def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), trac
                 st[1], st[3] = st[3], st[1]
     else:
         for n in range(n_steps):
-            step_blocks(blocks, exchange, states, dt)
+            step_blocks(blocks, exchange, states, dt,
+                        peers=peer_views(blocks, states) if peer else None)
             if track_from is not None and n >= track_from:
                 for st in states:
                     steady = max(steady, float((st[2] - st[0]).abs().max()))
@@ -464,4 +540,5 @@ def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), trac
 
 
 __all__ = ["HaloPlan", "make_plans", "DistExchange", "LoopbackExchange", "BlockStepper",
-           "halo_buffers", "step_blocks", "CapturedSteps", "run_parallel_2d", "SLOTS", "OPPOSITE"]
+           "halo_buffers", "step_blocks", "peer_views", "enable_peer_access", "CapturedSteps",
+           "run_parallel_2d", "SLOTS", "OPPOSITE"]

@@ -253,11 +253,15 @@ def _parallel_problem(nx, ny, nv, faces, seed):
     return mesh, BoundarySpec2D(*faces), CollisionModel("esbgk_2d", nu=-0.5), Q, G
 
 
+@pytest.mark.parametrize("halo", ["peer", "packed"])
 @pytest.mark.parametrize("nv", [6, 32])
 @pytest.mark.parametrize("grid,faces", [
     ((2, 2), "cavity"), ((3, 4), "cavity"), ((2, 2), "periodic"), ((4, 3), "mixed"),
-    ((1, 1), "periodic"), ((2, 1), "periodic"), ((1, 3), "cavity")])
-def test_block_grid_equals_serial_bitwise(mm, grid, faces, nv):
+    ((1, 1), "periodic"), ((2, 1), "periodic"), ((1, 3), "cavity"), ((3, 2), "periodic"),
+    ((1, 2), "periodic")])
+def test_block_grid_equals_serial_bitwise(mm, grid, faces, nv, halo):
+    """Both forms of the G halo: "peer" (ghost cells read in place from the
+    neighbour blocks' arrays) and "packed" (pack, copy, receive)."""
     from paper_2509_21832_b200 import EXTRAPOLATE, PERIODIC, WallSpec
     from paper_2509_21832_b200.parallel import run_parallel_2d
     w = WallSpec(1.0)
@@ -265,7 +269,7 @@ def test_block_grid_equals_serial_bitwise(mm, grid, faces, nv):
           "mixed": (EXTRAPOLATE, EXTRAPOLATE, PERIODIC, PERIODIC)}[faces]
     mesh, bc, model, Q0, G0 = _parallel_problem(12, 12, nv, fc, 11)
     dt = 0.3 * (1.0 / 12) / 5.0
-    Qp, Gp, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, 6, grid=grid)
+    Qp, Gp, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, 6, grid=grid, halo=halo)
     st = mm.State2D(0.0, Q0, G0)
     for _ in range(6):
         st = mm.step_2d(st, mesh, bc, 0.08, model, dt)
@@ -273,8 +277,9 @@ def test_block_grid_equals_serial_bitwise(mm, grid, faces, nv):
     assert np.array_equal(Gp, st.G)
 
 
+@pytest.mark.parametrize("halo", ["peer", "packed"])
 @pytest.mark.parametrize("nsteps", [1, 5])
-def test_block_grid_graph_replay_equals_eager(mm, nsteps):
+def test_block_grid_graph_replay_equals_eager(mm, nsteps, halo):
     """run_parallel_2d's CUDA-graph replay of the decomposed step (blocks on
     one GPU) is bitwise its eager issue and the serial step, for an odd step
     count too (the ping-pong parity)."""
@@ -283,9 +288,10 @@ def test_block_grid_graph_replay_equals_eager(mm, nsteps):
     w = WallSpec(1.0)
     mesh, bc, model, Q0, G0 = _parallel_problem(12, 12, 32, (PERIODIC, PERIODIC, w, w), 5)
     dt = 0.3 * (1.0 / 12) / 5.0
-    Qg, Gg, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, nsteps, grid=(2, 3))
+    Qg, Gg, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, nsteps, grid=(2, 3),
+                                   halo=halo)
     Qe, Ge, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, nsteps, grid=(2, 3),
-                                   graph=False)
+                                   graph=False, halo=halo)
     st = mm.State2D(0.0, Q0, G0)
     for _ in range(nsteps):
         st = mm.step_2d(st, mesh, bc, 0.08, model, dt)
@@ -358,9 +364,10 @@ def test_v1024_band_layout_is_bitwise_neutral(mm, bands, monkeypatch):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("halo", ["packed", "peer"])
 @pytest.mark.parametrize("nv", [6, 32])
 @pytest.mark.parametrize("faces,eps", [("periodic", 0.08), ("mixed", 0.08), ("periodic", 1e-12)])
-def test_block_grid_overlap_split_equals_serial(mm, faces, eps, nv):
+def test_block_grid_overlap_split_equals_serial(mm, faces, eps, nv, halo):
     """Blocks tall and wide enough that every split has interior micro CTAs
     (run while the G halo is in flight) and perimeter CTAs (a separate
     launch on a side stream): the decomposed step stays bitwise the serial
@@ -372,7 +379,7 @@ def test_block_grid_overlap_split_equals_serial(mm, faces, eps, nv):
           "mixed": (EXTRAPOLATE, EXTRAPOLATE, PERIODIC, PERIODIC)}[faces]
     mesh, bc, model, Q0, G0 = _parallel_problem(24, 400, nv, fc, 13)
     dt = 0.3 * (1.0 / 400) / 5.0
-    Qp, Gp, _, _ = run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, 3, grid=(2, 2))
+    Qp, Gp, _, _ = run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, 3, grid=(2, 2), halo=halo)
     st = mm.State2D(0.0, Q0, G0)
     for _ in range(3):
         st = mm.step_2d(st, mesh, bc, eps, model, dt)

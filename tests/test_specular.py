@@ -215,8 +215,9 @@ def test_gpu_specular_block_grid_equals_serial_bitwise(mm, grid, nv):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("halo", ["packed", "peer"])
 @pytest.mark.parametrize("nv", [6, 32])
-def test_gpu_specular_overlap_split_equals_serial(mm, nv):
+def test_gpu_specular_overlap_split_equals_serial(mm, nv, halo):
     """Blocks large enough that the split micro launch has interior CTAs
     (run while the G halo is in flight) and perimeter CTAs, with specular
     faces on the physical boundary: still bitwise the serial step."""
@@ -226,7 +227,7 @@ def test_gpu_specular_overlap_split_equals_serial(mm, nv):
     mesh, bc, model = _problem(nx, ny, (S, S, S, S), nv=nv, vmax=5.0)
     Q0, G0 = _state(nx, ny, nv, seed=12, amp=1e-2)
     dt = 0.3 * (1.0 / ny) / 5.0
-    Qp, Gp, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, 3, grid=(2, 2))
+    Qp, Gp, _, _ = run_parallel_2d(mesh, bc, 0.08, model, Q0, G0, dt, 3, grid=(2, 2), halo=halo)
     st = mm.State2D(0.0, Q0, G0)
     for _ in range(3):
         st = mm.step_2d(st, mesh, bc, 0.08, model, dt)
