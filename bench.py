@@ -503,7 +503,7 @@ def run_ours_multi(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2509_21832_b200 import _native
-    from paper_2509_21832_b200.parallel import (BlockStepper, DistExchange, make_plans,
+    from paper_2509_21832_b200.parallel import (BlockStepper, DistExchange, IpcPeers, make_plans,
                                                 step_blocks)
     gloo = args.backend == "gloo"
     if gloo:
@@ -526,17 +526,42 @@ def run_ours_multi(args, rank, world, local_rank):
     lib = _native.load()
     bx, by = plan.shape
     Q = torch.from_numpy(cfg["initial"](plan.i0, plan.i1, plan.j0, plan.j1)).cuda()
-    G = torch.zeros((bx, by, 32, 32), dtype=torch.float64, device="cuda")
-    st = [Q, G, torch.empty_like(Q), torch.empty_like(G),
+    # peer form of the G halo: every rank maps its neighbours' G buffers
+    # (CUDA IPC) and its micro kernel reads the ghost cells in place over
+    # NVLink; all ranks must agree, so one failed mapping selects the packed
+    # NCCL ring everywhere
+    peers = None
+    if args.halo == "peer" and any(s is not None for s in plan.slots):
+        try:
+            peers = IpcPeers(blk.solver, plan, (bx, by, 32, 32))
+            ok = 1
+        except RuntimeError:
+            ok = 0
+        flag = torch.tensor([ok], device="cpu" if gloo else "cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not int(flag.item()):
+            if peers is not None:
+                peers.close()
+            peers = None
+    if peers is not None:
+        G, Gb = peers.tensors
+        G.zero_()
+    else:
+        G = torch.zeros((bx, by, 32, 32), dtype=torch.float64, device="cuda")
+        Gb = torch.empty_like(G)
+    st = [Q, G, torch.empty_like(Q), Gb,
           torch.empty((4, bx, by), dtype=torch.float64, device="cuda")]
     dt = cfg["dt"]
+    par = [0]
     dist.barrier()
 
     def steps(n):
         for _ in range(n):
-            step_blocks([blk], exch, [st], dt)
+            step_blocks([blk], exch, [st], dt,
+                        peers=[peers.views(par[0])] if peers is not None else None)
             st[0], st[2] = st[2], st[0]
             st[1], st[3] = st[3], st[1]
+            par[0] ^= 1
 
     steps(args.warmup)
     torch.cuda.synchronize()
@@ -602,8 +627,10 @@ def run_ours_multi(args, rank, world, local_rank):
         "config": public_config(cfg, world, px, py),
         "exchange": ("gloo via pinned host (functional test only)" if gloo else
                      "NCCL send/recv (torch.distributed)") +
-                    ", Q ring, then the G ring overlapped with the interior micro CTAs, "
-                    "then the heat ring, per step",
+                    (", Q ring, G ghost cells read in place from the neighbours' arrays "
+                     "(CUDA-IPC peer memory), then the heat ring, per step" if peers is not None
+                     else ", Q ring, then the G ring overlapped with the interior micro CTAs, "
+                          "then the heat ring, per step"),
         "roofline": {"bound": "hbm", "kernel": "full decomposed step",
                      "achieved": step_gbs / world, "peak": peak, "unit": "GB/s",
                      "frac": step_gbs / world / peak, "traffic": None, "peak_source": peak_src,
@@ -617,6 +644,9 @@ def run_ours_multi(args, rank, world, local_rank):
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.barrier()
+    if peers is not None:
+        del st, G, Gb
+        peers.close()
     dist.destroy_process_group()
 
 
@@ -889,6 +919,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional test of the multi-rank path on fewer GPUs than ranks")
+    ap.add_argument("--halo", default="peer", choices=["peer", "packed"],
+                    help="multi-GPU G halo: peer = ghost cells read in place from the neighbours' "
+                         "arrays over NVLink (CUDA IPC); packed = packed NCCL ring")
     ap.add_argument("--eps", type=float, default=None, help="override the config's Knudsen number")
     ap.add_argument("--seed", type=int, default=0, help="C5 initial-condition seed")
     ap.add_argument("--serial-steps", type=int, default=3,

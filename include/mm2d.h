@@ -201,6 +201,16 @@ int mm2d_halo_unpack(mm2d_ctx *ctx, int which, void *stream);
 int mm2d_halo_peer(mm2d_ctx *ctx, const double *const *d_nbG);
 int mm2d_enable_peer_access(int device, int peer_device);
 
+/* One process per GPU: state arrays a neighbour process can map.
+ * mm2d_ipc_alloc: a cudaMalloc allocation on the current device plus its
+ * 64-byte CUDA-IPC handle; mm2d_ipc_open maps another process's allocation
+ * (peer access enabled lazily) and returns the pointer to pass to
+ * mm2d_halo_peer; close / free release them. */
+int mm2d_ipc_alloc(long long bytes, void **d_ptr, unsigned char *handle64);
+int mm2d_ipc_open(const unsigned char *handle64, void **d_ptr);
+int mm2d_ipc_close(void *d_ptr);
+int mm2d_ipc_free(void *d_ptr);
+
 /* ---- the ten kernel-contract functions (_kernels plugin API) ----
  * device pointers, reference layouts; `ext` arrays carry one ghost layer on
  * the differenced axis. */

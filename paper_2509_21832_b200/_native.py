@@ -100,6 +100,10 @@ SIGNATURES = {
     "mm2d_halo_unpack": (C.c_int, [_vp, C.c_int, _vp]),
     "mm2d_halo_peer": (C.c_int, [_vp, C.POINTER(_vp)]),
     "mm2d_enable_peer_access": (C.c_int, [C.c_int, C.c_int]),
+    "mm2d_ipc_alloc": (C.c_int, [C.c_longlong, C.POINTER(_vp), C.c_char_p]),
+    "mm2d_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "mm2d_ipc_close": (C.c_int, [_vp]),
+    "mm2d_ipc_free": (C.c_int, [_vp]),
     "mm2d_k_maxwellian_field_2d": (C.c_int, [C.c_int] * 4 + [_vp] * 7 + [_vp]),
     "mm2d_k_project_field_2d": (C.c_int, [C.c_int] * 4 + [_vp] * 8 + [C.c_double, _vp, _vp]),
     "mm2d_k_transport_stage_2d": (C.c_int, [C.c_int] * 4 + [_vp] * 8 +

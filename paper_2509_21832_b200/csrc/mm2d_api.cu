@@ -1126,6 +1126,44 @@ extern "C" int mm2d_enable_peer_access(int device, int peer_device) {
     return e == cudaSuccess ? MM2D_OK : MM2D_ERR_INTERNAL;
 }
 
+// Device arrays another process can map (one process per GPU): plain
+// cudaMalloc allocations with their CUDA-IPC handle (64 bytes).
+extern "C" int mm2d_ipc_alloc(long long bytes, void** d_ptr, unsigned char* handle64) {
+    if (!d_ptr || !handle64 || bytes <= 0) return MM2D_ERR_CONFIG;
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    void* p = nullptr;
+    if (cudaMalloc(&p, (size_t)bytes) != cudaSuccess) return MM2D_ERR_INTERNAL;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+        cudaFree(p);
+        return MM2D_ERR_INTERNAL;
+    }
+    memcpy(handle64, &h, 64);
+    *d_ptr = p;
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_ipc_open(const unsigned char* handle64, void** d_ptr) {
+    if (!d_ptr || !handle64) return MM2D_ERR_CONFIG;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return MM2D_ERR_INTERNAL;
+    }
+    *d_ptr = p;
+    return MM2D_OK;
+}
+
+extern "C" int mm2d_ipc_close(void* d_ptr) {
+    return cudaIpcCloseMemHandle(d_ptr) == cudaSuccess ? MM2D_OK : MM2D_ERR_INTERNAL;
+}
+
+extern "C" int mm2d_ipc_free(void* d_ptr) {
+    return cudaFree(d_ptr) == cudaSuccess ? MM2D_OK : MM2D_ERR_INTERNAL;
+}
+
 extern "C" int mm2d_halo_pack(mm2d_ctx* ctx, int which, const double* d_src, void* stream) {
     if (!ctx || which < 0 || which > 2) return fail_cfg(ctx, "bad halo field");
     CK(cudaSetDevice(ctx->dev));

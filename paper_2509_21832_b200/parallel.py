@@ -298,6 +298,7 @@ class BlockStepper:
             self.side = torch.cuda.Stream(device)   # the perimeter micro CTAs of a split step
             self.ev_prep = torch.cuda.Event()
             self.ev_side = torch.cuda.Event()
+        self.peer_on = False
 
     def _stream(self):
         import torch
@@ -318,6 +319,7 @@ class BlockStepper:
         current G tensor (or raw device pointer) of the neighbour in slot s,
         None for an inactive slot; ``None`` returns to the packed form."""
         s = self.solver
+        self.peer_on = neigh_G is not None
         if neigh_G is None:
             s._rc(s.lib.mm2d_halo_peer(s.ctx, None))
             return
@@ -368,6 +370,62 @@ def _step_blocks_peer(blocks, exchange, states, dt, peers):
             b.phase(1, st[0], st[1], dt, st[2], st[3], st[4])
 
 
+class IpcPeers:
+    """Peer form of the G halo with one process per GPU: this rank's two G
+    buffers (the step's ping-pong) are cudaMalloc allocations whose CUDA-IPC
+    handles every rank gathers; each rank maps its neighbours' buffers and
+    passes the pair that holds their G^n to mm2d_halo_peer every step.  All
+    ranks swap buffers together, so ``views(parity)`` of step n uses parity
+    n % 2 on every rank."""
+
+    def __init__(self, solver, plan: HaloPlan, shape, group=None):
+        import torch
+        import torch.distributed as dist
+        self.lib, self.device = solver.lib, solver.device
+        n = int(np.prod(shape))
+        self.own, handles = [], []
+        with torch.cuda.device(self.device):
+            for _ in range(2):
+                p, h = C.c_void_p(), C.create_string_buffer(64)
+                if self.lib.mm2d_ipc_alloc(8 * n, C.byref(p), h) != 0:
+                    raise RuntimeError("mm2d_ipc_alloc failed")
+                handles.append(h.raw)
+                self.own.append(p.value)
+            self.tensors = [torch.as_tensor(_CAI(p, n), device=self.device).view(shape)
+                            for p in self.own]
+        rank = dist.get_rank(group)
+        gathered = [None] * dist.get_world_size(group)
+        dist.all_gather_object(gathered, (rank, handles), group=group)
+        table = dict(gathered)
+        self.mapped = {}
+        with torch.cuda.device(self.device):
+            for nb in sorted({s for s in plan.slots if s is not None}):
+                ptrs = []
+                for h in table[nb]:
+                    p = C.c_void_p()
+                    if self.lib.mm2d_ipc_open(h, C.byref(p)) != 0:
+                        raise RuntimeError(f"mm2d_ipc_open failed for rank {nb}")
+                    ptrs.append(p.value)
+                self.mapped[nb] = ptrs
+        self.slots = plan.slots
+
+    def views(self, parity):
+        return [None if nb is None else self.mapped[nb][parity] for nb in self.slots]
+
+    def close(self):
+        import torch
+        with torch.cuda.device(self.device):
+            torch.cuda.synchronize()
+            for ptrs in self.mapped.values():
+                for p in ptrs:
+                    self.lib.mm2d_ipc_close(C.c_void_p(p))
+            self.mapped = {}
+            self.tensors = []
+            for p in self.own:
+                self.lib.mm2d_ipc_free(C.c_void_p(p))
+            self.own = []
+
+
 def step_blocks(blocks, exchange, states, dt, peers=None):
     """One decomposed step for every block held by this process.
     ``states[b] = (Q, G, Qout, Gout, H)`` device tensors of block b.
@@ -388,6 +446,8 @@ def step_blocks(blocks, exchange, states, dt, peers=None):
         return _step_blocks_peer(blocks, exchange, states, dt, peers)
     for b, st in zip(blocks, states):
         with torch.cuda.device(b.solver.device):
+            if b.peer_on:
+                b.set_peers(None)
             b.pack(FIELD_Q, st[0])
             b.pack(FIELD_G, st[1])
     exchange.exchange(FIELD_Q)
@@ -540,5 +600,6 @@ def run_parallel_2d(mesh, bc, eps, model, Q0, G0, dt, n_steps, grid=(2, 2), trac
 
 
 __all__ = ["HaloPlan", "make_plans", "DistExchange", "LoopbackExchange", "BlockStepper",
-           "halo_buffers", "step_blocks", "peer_views", "enable_peer_access", "CapturedSteps",
+           "halo_buffers", "step_blocks", "peer_views", "enable_peer_access", "IpcPeers",
+           "CapturedSteps",
            "run_parallel_2d", "SLOTS", "OPPOSITE"]

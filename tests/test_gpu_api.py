@@ -132,3 +132,22 @@ def test_multirank_bench_path_over_gloo(mm):
     d = lines[0]
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "dd2x1"
     assert d["gpu_launches"] > 0
+
+
+@pytest.mark.parametrize("grid,faces,halo", [((2, 1), "periodic", "peer"), ((2, 2), "periodic", "peer"),
+                                             ((2, 2), "cavity", "peer"), ((1, 2), "mixed", "peer"),
+                                             ((2, 2), "periodic", "packed")])
+def test_one_process_per_block_equals_serial_bitwise(mm, grid, faces, halo):
+    """One process per block (torchrun, gloo-staged Q / H rings, every rank on
+    this GPU): with the G ghost cells read in place from the neighbour
+    PROCESSES' arrays (CUDA-IPC mappings, IpcPeers) the decomposed run is
+    bitwise the serial step_2d; likewise with the packed G ring."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    n = grid[0] * grid[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29741",
+           str(ROOT / "tools" / "multirank_check.py"), "--grid", str(grid[0]), str(grid[1]),
+           "--halo", halo, "--faces", faces]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, (r.stdout[-1500:], r.stderr[-1500:])
+    assert "BITWISE OK" in r.stdout, r.stdout

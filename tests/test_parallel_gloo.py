@@ -209,6 +209,11 @@ def test_step_blocks_overlaps_g_exchange_with_interior_micro(monkeypatch):
         side = Stream("side")
         ev_prep = Event("prep")
         ev_side = Event("side")
+        peer_on = False
+
+        def set_peers(self, nb):
+            self.peer_on = nb is not None
+            log.append(("peers", None if nb is None else tuple(nb)))
 
         class solver:
             device = torch.device("cpu")
@@ -240,3 +245,35 @@ def test_step_blocks_overlaps_g_exchange_with_interior_micro(monkeypatch):
                    ("wait", "side", "prep"), ("finish", G, "side"), ("phase", 3, "side"),
                    ("record", "side"), ("wait", "main", "side"), ("pack", H),
                    ("exchange", H), ("unpack", H), ("phase", 1, "main")]
+
+    # peer form of the G halo: no G pack / exchange; the Q ring (which orders
+    # the step against the neighbours) comes before the one micro launch
+    # (phase 0) that reads the neighbours' arrays in place
+    del log[:]
+    blk = Blk()
+    nb = [101, 102, None, None, None, None, None, None]
+    par.step_blocks([blk], Ex(), [(None,) * 5], 1e-3, peers=[nb])
+    assert log == [("peers", tuple(nb)), ("pack", Q), ("exchange", Q), ("unpack", Q),
+                   ("phase", 0, "main"), ("pack", H), ("exchange", H), ("unpack", H),
+                   ("phase", 1, "main")]
+    # and a later packed step first returns the context to the packed form
+    del log[:]
+    par.step_blocks([blk], Ex(), [(None,) * 5], 1e-3)
+    assert log[0] == ("peers", None) and log[1:3] == [("pack", Q), ("pack", G)]
+
+
+def test_peer_views_follow_the_plans_slots():
+    """peer_views: per block, the current G of the neighbour in each of the 8
+    slots (None where the slot is a physical face or wraps locally)."""
+    from paper_2509_21832_b200 import BoundarySpec2D, EXTRAPOLATE, PERIODIC
+    from paper_2509_21832_b200.parallel import make_plans, peer_views
+    from types import SimpleNamespace as NS
+    plans = make_plans(8, 8, (2, 2), BoundarySpec2D(EXTRAPOLATE, EXTRAPOLATE, PERIODIC, PERIODIC))
+    blocks = [NS(plan=p) for p in plans]
+    states = [[None, f"G{p.rank}", None, None, None] for p in plans]
+    views = peer_views(blocks, states)
+    for p, v in zip(plans, views):
+        assert v == [None if nb is None else f"G{nb}" for nb in p.slots]
+    # rank 0 = block (0, 0): no left neighbour (extrapolate), right = rank 2,
+    # bottom and top = rank 1 (periodic over two blocks in y)
+    assert views[0][0] is None and views[0][1] == "G2" and views[0][2] == "G1" and views[0][3] == "G1"
