@@ -108,16 +108,17 @@ __device__ __forceinline__ bool err_pending(const unsigned long long* w, int pre
 
 // Per-ring-cell parameters produced by the prep kernel (all from Q^n).
 struct __align__(16) CellPar {
-    double rho, u1, u2, T;           // 0-3   primitives (gas_state.py:93-108)
-    double isT, tau, pref, inv2T;    // 4-7   1/sqrt(T), tau, rho/(2 pi T), 1/(2T)
-    double s11, s12, gT1, gT2;       // 8-11  sigma and grad T (micro2d.py:37-60)
-    double t11, t12, t22, invT;      // 12-15 temperature tensor, 1/T
-    double scale, wg, wh, invtau;    // 16-19 dv/rho, relax weights, 1/tau
-    double gpref, gq11, gq22, gq12;  // 20-23 Gaussian: rho/(2 pi sqrt det), c22/det, c11/det, c12/det
-    double rw[4];                    // 24-27 diffuse-wall ghost densities (left,right,bottom,top)
-    double m11, m12, m22, pad;       // 28-31 modified tensor (gas_state.py:138-146)
+    double u1, u2, isT, tau;            // 0-3   velocity (gas_state.py:93-108), 1/sqrt(T), tau
+    double pref, inv2T, invT, scale;    // 4-7   rho/(2 pi T), 1/(2T), 1/T, dv/rho
+    double s11, s12, gT1, gT2;          // 8-11  sigma and grad T (micro2d.py:37-60)
+    double wg, wh, invtau, gpref;       // 12-15 relax weights, 1/tau, Gaussian rho/(2 pi sqrt det)
+    double gq11, gq22, gq12, pad;       // 16-19 Gaussian exponents c22/det, c11/det, c12/det
+    double rw[4];                       // 20-23 diffuse-wall ghost densities (left,right,bottom,top)
 };
-static_assert(sizeof(CellPar) == 32 * sizeof(double), "CellPar layout");
+// (round 1's 32-double layout also carried rho, T, the temperature tensor and
+// the modified tensor, which no kernel reads: a quarter of the prep's writes)
+constexpr int kParD = 24;               // doubles per CellPar
+static_assert(sizeof(CellPar) == kParD * sizeof(double), "CellPar layout");
 
 struct Geometry {
     int bx, by;          // local block

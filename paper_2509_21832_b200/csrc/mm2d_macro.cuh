@@ -128,11 +128,22 @@ __device__ __forceinline__ void kfvs_half(const double* s, double sgn, double* o
 // its neighbours' (3 relaxations and 4 half fluxes per cell before).  The
 // interface flux keeps the expression (0 + L_left) + R_right, so results are
 // bitwise those of the untiled kernels.
-constexpr int MX_TI = 8;                 // output cells per CTA along x
+#ifndef MM2D_MX_TI
+#define MM2D_MX_TI 8
+#endif
+#ifndef MM2D_MX_MINB
+#define MM2D_MX_MINB 0   // 0: no minimum (58 registers, the fastest: 0.294 ms at C5; 6 -> 0.318, tiles of 12 -> 0.320)
+#endif
+#if MM2D_MX_MINB > 0
+#define MM2D_MX_BOUNDS __launch_bounds__(MX_TJ * (MX_TI + 2), MM2D_MX_MINB)
+#else
+#define MM2D_MX_BOUNDS __launch_bounds__(MX_TJ * (MX_TI + 2))
+#endif
+constexpr int MX_TI = MM2D_MX_TI;        // output cells per CTA along x
 constexpr int MX_TJ = 32;                // cells per CTA along y (one warp row)
 
 // x-sweep: block (32, MX_TI + 2); thread (lane, r) owns cell (i0 - 1 + r, j)
-__global__ void __launch_bounds__(MX_TJ * (MX_TI + 2)) k_macro_x(MacroArgs a) {
+__global__ void MM2D_MX_BOUNDS k_macro_x(MacroArgs a) {
     pdl_enter();
     __shared__ double sL[MX_TI + 2][6][MX_TJ], sR[MX_TI + 2][6][MX_TJ];
     const Geometry& g = a.g;
@@ -201,7 +212,10 @@ __global__ void __launch_bounds__(MX_TJ * (MX_TI + 2)) k_macro_x(MacroArgs a) {
 // y-sweep: one warp per 30 output cells along y; lane l owns cell
 // j0 - 1 + l and takes its neighbours' half fluxes by shuffles
 constexpr int MY_OUT = 30;
-__global__ void __launch_bounds__(128) k_macro_y(MacroArgs a) {
+#ifndef MM2D_MY_MINB
+#define MM2D_MY_MINB 8   // 64 registers (a few spills): 0.273 -> 0.230 ms at C5; 6: 0.247
+#endif
+__global__ void __launch_bounds__(128, MM2D_MY_MINB) k_macro_y(MacroArgs a) {
     pdl_enter();
     const Geometry& g = a.g;
     if (err_gate(a.err, EW_MX)) return;

@@ -230,8 +230,8 @@ __device__ __forceinline__ void build_row(const MicroArgs& a, const RowTables<BX
                                           int r, const double* v1s, const double* v2s) {
     const Geometry& g = a.g;
     const int nv1 = g.nv1, nv2 = g.nv2;
-    for (int q = threadIdx.x; q < BX * 32; q += blockDim.x) {
-        const int b = q >> 5, c = q & 31;
+    for (int q = threadIdx.x; q < BX * kParD; q += blockDim.x) {
+        const int b = q / kParD, c = q - b * kParD;
         const int i = min(ic0 + b, g.bx - 1);
         reinterpret_cast<double*>(t.par)[q] =
             reinterpret_cast<const double*>(a.P + ring_index(g, i, r))[c];

@@ -31,7 +31,7 @@
 // version of this kernel: bump on every change that alters its code, so
 // committed ncu captures (profiles/micro_traffic.json) stay tied to it
 #ifndef M32_KERNEL_VERSION
-#define M32_KERNEL_VERSION 29
+#define M32_KERNEL_VERSION 30
 #endif
 
 // Projection sums in raw velocity moments (v28).  1: each thread weights its
@@ -812,10 +812,10 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     const int rhi = k_hi == 0 ? j1s : j1s - 1;
     auto computes = [&](int r) { return (unsigned)(r - rlo) <= (unsigned)(rhi - rlo); };
 
-    // CellPar of ring row r -> pring[r & 3], 16 threads x 16 bytes; one
+    // CellPar of ring row r -> pring[r & 3], 12 threads x 16 bytes; one
     // commit group per call so wait_group 1 leaves exactly the newest in flight
     auto stage_par = [&](int r, bool on) {
-        if (on && tid < 16)
+        if (on && tid < kParD / 2)
             cp_async16(pring + 32 * (r & 3) + 2 * tid,
                        reinterpret_cast<const double*>(a.P + ring_index(g, i, r)) + 2 * tid);
         cp_async_commit();

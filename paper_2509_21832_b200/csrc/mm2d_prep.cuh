@@ -213,8 +213,7 @@ __device__ __forceinline__ void prep_cell(const PrepArgs& a, int t, int i, int j
             const double det = t11 * t22 - t12 * t12;
             if ((t11 <= tol) || (det <= tol * tol)) atomicMin(a.err + EW_PREP, err_key(a.step, ES_PRIM_SPD, gcell));
         }
-        P.rho = rho; P.u1 = u1; P.u2 = u2; P.T = T;
-        P.t11 = t11; P.t12 = t12; P.t22 = t22;
+        P.u1 = u1; P.u2 = u2;
         // reciprocals shared between the derived constants (each division
         // costs ~40 instructions with its slow-path guard)
         const double invT = 1.0 / T;
@@ -230,7 +229,6 @@ __device__ __forceinline__ void prep_cell(const PrepArgs& a, int t, int i, int j
         P.wg = a.eps * rden;
         P.wh = a.dt * tau * rden;
         P.s11 = P.s12 = P.gT1 = P.gT2 = 0.0;
-        P.m11 = P.m12 = P.m22 = 0.0;
         P.gpref = P.gq11 = P.gq22 = P.gq12 = 0.0;
         P.rw[0] = P.rw[1] = P.rw[2] = P.rw[3] = 0.0;
         P.pad = 0.0;
@@ -240,7 +238,6 @@ __device__ __forceinline__ void prep_cell(const PrepArgs& a, int t, int i, int j
             const double m22 = (1.0 - a.nu) * T + a.nu * t22;
             const double det = m11 * m22 - m12 * m12;
             const double rdet = 1.0 / det;
-            P.m11 = m11; P.m12 = m12; P.m22 = m22;
             P.gpref = rho * (0.5 / kPi) * rsqrt(det);
             P.gq11 = -0.5 * m22 * rdet;  // coefficient of W1^2 in the exponent
             P.gq22 = -0.5 * m11 * rdet;  // coefficient of W2^2
@@ -324,12 +321,14 @@ __global__ void k_prep(PrepArgs a) {
 #define MM2D_PREP_TI 4   // tile rows (warps per CTA); 4 measured faster than 8
 #endif
 constexpr int PT_I = MM2D_PREP_TI, PT_J = 32, PT_THREADS = PT_I * PT_J;
-constexpr size_t kPrepStageBytes = sizeof(CellPar) * PT_THREADS;
+constexpr size_t kPrepStageBytes = sizeof(double) * 32 * PT_THREADS;   // 32-double rows (swizzled)
 
 __device__ __forceinline__ int prep_tiles(const Geometry& g) {
     return ((g.bx + 2 + PT_I - 1) / PT_I) * ((g.by + 2 + PT_J - 1) / PT_J);
 }
 
+// (resident-CTA minimums measured slower: 6 -> +5 %, 8 -> +15 %; an explicit 1 lets
+// ptxas take more registers and is slower too)
 __global__ void __launch_bounds__(PT_THREADS) k_prep_tiled(PrepArgs a) {
     pdl_enter();
     const Geometry& g = a.g;
@@ -364,7 +363,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_prep_tiled(PrepArgs a) {
                 // stage with an XOR swizzle (bank = e ^ lane: conflict-free)
                 const double* pv = reinterpret_cast<const double*>(&P);
 #pragma unroll
-                for (int e = 0; e < 32; ++e) st[e ^ lj] = pv[e];
+                for (int e = 0; e < kParD; ++e) st[e ^ lj] = pv[e];
             });
         }
         __syncwarp();
@@ -372,10 +371,10 @@ __global__ void __launch_bounds__(PT_THREADS) k_prep_tiled(PrepArgs a) {
         // 512-byte coalesced runs of double2
         if (ri < g.bx + 2) {
             MM2D_CHECK(rj0 + nrow <= g.by + 2 && nrow > 0);
-            double* dst = reinterpret_cast<double*>(a.P) + ((size_t)ri * (g.by + 2) + rj0) * 32;
+            double* dst = reinterpret_cast<double*>(a.P) + ((size_t)ri * (g.by + 2) + rj0) * kParD;
             const double* wst = stage + (threadIdx.x - lj) * 32;
-            for (int f = 2 * lj; f < nrow * 32; f += 64) {
-                const int c = f >> 5, e = f & 31;
+            for (int f = 2 * lj; f < nrow * kParD; f += 64) {
+                const int c = f / kParD, e = f - c * kParD;
                 const double x0 = wst[c * 32 + (e ^ c)], x1 = wst[c * 32 + ((e + 1) ^ c)];
                 *reinterpret_cast<double2*>(dst + f) = make_double2(x0, x1);
             }
