@@ -129,7 +129,7 @@ __device__ __forceinline__ void kfvs_half(const double* s, double sgn, double* o
 // interface flux keeps the expression (0 + L_left) + R_right, so results are
 // bitwise those of the untiled kernels.
 #ifndef MM2D_MX_TI
-#define MM2D_MX_TI 8
+#define MM2D_MX_TI 10   // tile rows along x: 6 / 8 / 10 / 12 / 14 -> 0.263 / 0.295 / 0.255 / 0.314 / 0.285 ms at C5
 #endif
 #ifndef MM2D_MX_MINB
 #define MM2D_MX_MINB 0   // 0: no minimum (58 registers, the fastest: 0.294 ms at C5; 6 -> 0.318, tiles of 12 -> 0.320)
