@@ -532,16 +532,14 @@ def run_ours_multi(args, rank, world, local_rank):
     # NCCL ring everywhere
     peers = None
     if args.halo == "peer" and any(s is not None for s in plan.slots):
-        try:
-            peers = IpcPeers(blk.solver, plan, (bx, by, 32, 32))
-            ok = 1
-        except RuntimeError:
-            ok = 0
-        flag = torch.tensor([ok], device="cpu" if gloo else "cuda")
+        peers = IpcPeers(blk.solver, plan, (bx, by, 32, 32))
+        flag = torch.tensor([0 if peers.failed else 1], device="cpu" if gloo else "cuda")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if not int(flag.item()):
-            if peers is not None:
-                peers.close()
+            if peers.failed and rank == 0:
+                print(f"bench: peer-form halo unavailable ({peers.failed}); packed ring",
+                      file=sys.stderr)
+            peers.close()
             peers = None
     if peers is not None:
         G, Gb = peers.tensors

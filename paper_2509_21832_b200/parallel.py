@@ -381,38 +381,50 @@ class IpcPeers:
     def __init__(self, solver, plan: HaloPlan, shape, group=None):
         import torch
         import torch.distributed as dist
-        self.lib, self.device = solver.lib, solver.device
+        self.lib, self.device, self.group = solver.lib, solver.device, group
+        self.slots = plan.slots
+        self.failed = None          # why the peer form is unavailable on this rank
+        self.own, self.tensors, self.mapped = [], [], {}
         n = int(np.prod(shape))
-        self.own, handles = [], []
+        handles = []
         with torch.cuda.device(self.device):
             for _ in range(2):
                 p, h = C.c_void_p(), C.create_string_buffer(64)
                 if self.lib.mm2d_ipc_alloc(8 * n, C.byref(p), h) != 0:
-                    raise RuntimeError("mm2d_ipc_alloc failed")
+                    self.failed = "mm2d_ipc_alloc failed"
+                    break
                 handles.append(h.raw)
                 self.own.append(p.value)
-            self.tensors = [torch.as_tensor(_CAI(p, n), device=self.device).view(shape)
-                            for p in self.own]
+            if self.failed is None:
+                self.tensors = [torch.as_tensor(_CAI(p, n), device=self.device).view(shape)
+                                for p in self.own]
+        # (collective: every rank takes part, also one whose allocation failed)
         rank = dist.get_rank(group)
         gathered = [None] * dist.get_world_size(group)
-        dist.all_gather_object(gathered, (rank, handles), group=group)
+        dist.all_gather_object(gathered, (rank, handles if self.failed is None else None),
+                               group=group)
         table = dict(gathered)
-        self.mapped = {}
         with torch.cuda.device(self.device):
             for nb in sorted({s for s in plan.slots if s is not None}):
+                if self.failed is not None:
+                    break
+                if table[nb] is None:
+                    self.failed = f"rank {nb} exported no buffers"
+                    break
                 ptrs = []
                 for h in table[nb]:
                     p = C.c_void_p()
                     if self.lib.mm2d_ipc_open(h, C.byref(p)) != 0:
-                        raise RuntimeError(f"mm2d_ipc_open failed for rank {nb}")
+                        self.failed = f"mm2d_ipc_open failed for rank {nb}"
+                        break
                     ptrs.append(p.value)
                 self.mapped[nb] = ptrs
-        self.slots = plan.slots
 
     def views(self, parity):
         return [None if nb is None else self.mapped[nb][parity] for nb in self.slots]
 
-    def close(self):
+    def unmap(self):
+        """Close this rank's mappings of its neighbours' buffers."""
         import torch
         with torch.cuda.device(self.device):
             torch.cuda.synchronize()
@@ -420,7 +432,19 @@ class IpcPeers:
                 for p in ptrs:
                     self.lib.mm2d_ipc_close(C.c_void_p(p))
             self.mapped = {}
+
+    def close(self, collective=True):
+        """Collective: every rank unmaps its neighbours' buffers, then (after a
+        barrier, so no importer still holds a mapping) frees its own.  With
+        ``collective=False`` the caller provides that barrier (some ranks may
+        hold no IpcPeers, e.g. after a failed mapping)."""
+        import torch
+        import torch.distributed as dist
+        self.unmap()
+        with torch.cuda.device(self.device):
             self.tensors = []
+            if collective and dist.is_initialized():
+                dist.barrier(group=self.group)
             for p in self.own:
                 self.lib.mm2d_ipc_free(C.c_void_p(p))
             self.own = []

@@ -64,6 +64,7 @@ def main():
     peers = None
     if args.halo == "peer":
         peers = IpcPeers(blk.solver, plan, (bx, by, nv, nv))
+        assert peers.failed is None, peers.failed
         G, Gb = peers.tensors
         G.copy_(torch.from_numpy(np.ascontiguousarray(G0[plan.i0:plan.i1, plan.j0:plan.j1])))
     else:
