@@ -31,7 +31,7 @@
 // version of this kernel: bump on every change that alters its code, so
 // committed ncu captures (profiles/micro_traffic.json) stay tied to it
 #ifndef M32_KERNEL_VERSION
-#define M32_KERNEL_VERSION 30
+#define M32_KERNEL_VERSION 31
 #endif
 
 // Projection sums in raw velocity moments (v28).  1: each thread weights its
@@ -46,6 +46,18 @@
 // w1, w2, b4 from the tables).
 #ifndef M32_RAW
 #define M32_RAW 1
+#endif
+
+// Projection polynomial tabulated per cell (v31, needs M32_RAW).  Its value at a
+// node is (X(k) + Z(l)) M: the k part times the Maxwellian's k factor, AL[k] =
+// X(k) pE1[k], and the l part times its l factor, BE[l] = Z(l) E2[l], depend on
+// k or l alone.  1: the reducer warp that converts a stage's totals also writes
+// the 32 + 32 values into the row's K- and L-table (one lane per entry), and
+// every thread loads its four AL and two BE instead of evaluating them (19 fp64
+// operations per thread and stage, 16 of every 17 of them redundant across the
+// threads that share a k or an l).  0: v30, every thread evaluates its own.
+#ifndef M32_TABPROJ
+#define M32_TABPROJ M32_RAW
 #endif
 
 #ifndef MICRO32_MINB
@@ -82,8 +94,13 @@ constexpr int TSLOTS = 4;            // table slots (rows j..j+3; the slot rebui
 #endif
 #endif
 #if M32_RAW
+#if M32_TABPROJ
+constexpr int KW = M32_W1POW_TABLE ? 12 : 10;   // K-table entries per k
+constexpr int LR = 8;                           // L-table rows
+#else
 constexpr int KW = M32_W1POW_TABLE ? 8 : 6;     // K-table entries per k
 constexpr int LR = 6;                           // L-table rows
+#endif
 #else
 constexpr int KW = M32_W1POW_TABLE ? 12 : 10;   // K-table entries per k
 constexpr int LR = 8;
@@ -101,12 +118,13 @@ constexpr int TAB = XT + 5 * 16;     // 816 doubles per cell
 // by the upwind coefficient
 #if M32_RAW
 #if M32_W1POW_TABLE
-enum { K_PE1, K_W1, K_W12, K_W13, K_F0, K_F1, K_F2, K_PE1B };
+enum { K_PE1, K_W1, K_W12, K_W13, K_F0, K_F1, K_F2, K_PE1B, K_PEX, K_ALX, K_ALY, K_PADK };
 #else
-enum { K_PE1, K_W1, K_F0, K_F1, K_F2, K_PE1B };
+// (K_PEX, K_ALX): pE1 again next to the x-stage's AL, one 16-byte load in the recon
+enum { K_PE1, K_W1, K_F0, K_F1, K_F2, K_PE1B, K_PEX, K_ALX, K_ALY, K_PADK };
 #endif
 // L-table rows: E2, W2, E2 W2, E2 W2^2, f3 E2 W2^3
-enum { L_E2, L_W2, L_EW1, L_EW2, L_EW3, L_PAD };
+enum { L_E2, L_W2, L_EW1, L_EW2, L_EW3, L_PAD, L_BEX, L_BEY };
 #else
 #if M32_W1POW_TABLE
 enum { K_W1N, K_H1, K_PE1, K_W1, K_XW, K_XH, K_W12, K_W13, K_F0, K_F1, K_F2, K_PE1B };
@@ -308,7 +326,8 @@ template <int NT_>
 __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred, double* hdst,
                                              double hfac, const MicroArgs& a, const double* Ty,
                                              const double* Tx, unsigned long long* mbarB,
-                                             unsigned parityB) {
+                                             unsigned parityB, double* Tyw, double* Txw,
+                                             const double* v1s, const double* v2s) {
     constexpr int NS = NT_ >= 128 ? M32_NS : 4;  // segments per value (threads per value)
     constexpr int SEG = NT_ / NS;           // partials per (value, segment)
     constexpr int L2N = SEG / 2;            // double2 loads per segment
@@ -348,10 +367,28 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred, doub
             const double2 sw = lds2(hdr + H_SCALE);        // scale, wg
             double Cf[4];
             raw_to_coef(a, hdr, isy ? sw.x * sw.y : sw.x, N0, N1, N2, N3, Cf);
+#if M32_TABPROJ
+            // lane m tabulates the polynomial's k part at k = m and its l part at
+            // l = m, in the node coordinates the threads use (same expressions as
+            // their cx / cy, so the same doubles)
+            {
+                const int m = tid & 31;
+                double* Tw = isy ? Tyw : Txw;
+                const double v1m = v1s[m], v2m = v2s[m];
+                const double xi = (m < NV / 2 ? -a.dt : a.dt) * v1m * a.idx;
+                const double eta = (v2m < 0.0 ? -a.dt : a.dt) * v2m * a.idy;
+                const double X = fma(xi, fma(Cf[3], xi, m < NV / 2 ? -Cf[1] : Cf[1]), Cf[0]);
+                const double Z = eta * fma(Cf[3] * a.ryx, eta, v2m < 0.0 ? -Cf[2] : Cf[2]);
+                double* K = Tw + KT + KW * m;
+                K[isy ? K_ALY : K_ALX] = X * K[K_PE1];
+                Tw[LT + (isy ? L_BEY : L_BEX) * NV + m] = Z * Tw[LT + L_E2 * NV + m];
+            }
+#else
             if ((tid & 31) == 0) {
                 sts2(sred + 12 * NT_ + (isy ? 0 : 4), Cf[0], Cf[1]);
                 sts2(sred + 12 * NT_ + (isy ? 2 : 6), Cf[2], Cf[3]);
             }
+#endif
         } else if (act && seg == 0 && hdst) hdst[vid - 8] = hfac * acc;
 #else
         if (act && seg == 0) {
@@ -369,12 +406,14 @@ __device__ __forceinline__ void reduce12_end(double (&v)[12], double* sred, doub
 #else
     __syncthreads();
 #endif
+#if !(M32_RAW && M32_TABPROJ)
 #pragma unroll
     for (int q = 0; q < 8; q += 2) {
         const double2 x = lds2(sred + 12 * NT_ + q);
         v[q] = x.x;
         v[q + 1] = x.y;
     }
+#endif
 }
 
 // build the per-cell tables from the shared copy P of the cell's CellPar.
@@ -409,6 +448,9 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         sts2(K + K_F0, pe * fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
              pe * (mtw * ((W1 * P.s12 + q1 * P.gT2) * P.invT)));
         sts2(K + K_F2, pe * (mtw * ((p1 - P.s11) * P.inv2T)), pe);   // pE1 again: one 16-byte load in the target
+#if M32_TABPROJ
+        K[K_PEX] = pe;
+#endif
         if (m == 0) {
             sts2(T + HD + H_SCALE, P.scale, P.wg);
             sts2(T + HD + H_MTW, mtw, a.inveps * P.wh);
@@ -947,7 +989,9 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
     double* T2 = tabs + 2 * SLOT;
     double* T3 = tabs + 3 * SLOT;
 
+#if !M32_TABPROJ
     double ax[4] = {0, 0, 0, 0};   // x-projection sums of the pending row
+#endif
     double hs[4] = {0, 0, 0, 0};   // heat partial sums of the previous row
     double ty[2 * NP_];            // G* - dt Z_y of the current row
 #pragma unroll
@@ -1015,7 +1059,12 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
         if (ST || computes(rc)) {
             const double* T = T1;
             const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
-#if M32_RAW
+#if M32_TABPROJ
+            // the x-stage's projection polynomial, tabulated by the reducer warp
+            // one row ago: BE[l] here, (pE1, AL)[k] per pair below
+            const double2 bEx = lds2(T + LT + L_BEX * NV + lb);
+            const double bE0 = bEx.x, bE1 = bEx.y;
+#elif M32_RAW
             // projection polynomial of the x-stage totals at the thread's nodes,
             // split as (C0 + C1 s xi + C3 xi^2) + eta (C2 s' + C3 ryx eta)
             const double c2s = sflip(ax[2]), c3y = ax[3] * a.ryx;
@@ -1033,8 +1082,14 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             tm_ld8(R2, gst);
 #pragma unroll
             for (int p = 0; p < NP_; ++p) {
+#if M32_TABPROJ
+                const double2 pa = lds2(T + koff_(p) + K_PEX);   // pE1, AL
+                const double pe = pa.x, alp = pa.y;
+#else
                 const double pe = T[koff_(p) + K_PE1];
-#if M32_RAW
+#endif
+#if M32_TABPROJ
+#elif M32_RAW
                 const double alp =
                     fma(cx[p], fma(ax[3], cx[p], p < NP_ / 2 ? -ax[1] : ax[1]), ax[0]) * pe;
 #else
@@ -1266,12 +1321,14 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                                                                 : nullptr,
                           a.hfac
 #if !M32_TMEM_RED
-                          , a, T0, T2, mbar + 1, (unsigned)(j - jfirst) & 1
+                          , a, T0, T2, mbar + 1, (unsigned)(j - jfirst) & 1, T0, T2, v1s, v2s
 #endif
                           );
+#if !M32_TABPROJ
         if (do_x) {
             ax[0] = s[4]; ax[1] = s[5]; ax[2] = s[6]; ax[3] = s[7];
         }
+#endif
         // 5. G**(j), relax, store, heat partials
         hs[0] = hs[1] = hs[2] = hs[3] = 0.0;
         if (row_j) {
@@ -1280,7 +1337,10 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             const double* T = T0;
             const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
             const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
-#if M32_RAW
+#if M32_TABPROJ
+            const double2 bEy = lds2(T + LT + L_BEY * NV + lb);
+            const double bE0 = bEy.x, bE1 = bEy.y;
+#elif M32_RAW
             // (the y totals arrive as polynomial coefficients, scale and wg folded in)
             const double c2s = sflip(s[2]), c3y = s[3] * a.ryx;
             const double bE0 = cy0 * fma(c3y, cy0, c2s) * E2.x;
@@ -1308,7 +1368,9 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 w3.x = pw.y * pw.y;
                 w3.y = w3.x * pw.y;
 #endif
-#if M32_RAW
+#if M32_TABPROJ
+                const double alp = K[K_ALY];
+#elif M32_RAW
                 const double alp =
                     fma(cx[p], fma(s[3], cx[p], p < NP_ / 2 ? -s[1] : s[1]), s[0]) * pw.x;
 #else
