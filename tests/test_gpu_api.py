@@ -117,13 +117,21 @@ def test_error_cell_is_stable_across_later_steps(mm):
     assert np.isfinite(ok.Q).all()
 
 
+def _free_port():
+    """A TCP port nobody listens on right now (the rendezvous port of a test's torchrun)."""
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def test_multirank_bench_path_over_gloo(mm):
     """bench.run_ours_multi with 2 ranks (gloo, host-staged exchanges):
     the decomposed step loop, both exchanges, max-over-ranks timing and
     the JSON line."""
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29731", str(ROOT / "bench.py"),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "c2", "--backend", "gloo"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -145,7 +153,7 @@ def test_one_process_per_block_equals_serial_bitwise(mm, grid, faces, halo):
     env = dict(os.environ, MASTER_ADDR="127.0.0.1")
     n = grid[0] * grid[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29741",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            str(ROOT / "tools" / "multirank_check.py"), "--grid", str(grid[0]), str(grid[1]),
            "--halo", halo, "--faces", faces]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
