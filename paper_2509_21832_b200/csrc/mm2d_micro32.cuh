@@ -31,7 +31,7 @@
 // version of this kernel: bump on every change that alters its code, so
 // committed ncu captures (profiles/micro_traffic.json) stay tied to it
 #ifndef M32_KERNEL_VERSION
-#define M32_KERNEL_VERSION 31
+#define M32_KERNEL_VERSION 32
 #endif
 
 // Projection sums in raw velocity moments (v28).  1: each thread weights its
@@ -188,7 +188,7 @@ __device__ __forceinline__ void reduce16(double (&v)[16], double* sred) {
 
 // Row header stored in each table slot (doubles): per-cell scalars the node
 // loops need, so they come from shared memory instead of global loads.
-enum { H_SCALE, H_WG, H_MTW, H_MEW, H_GQ12, H_WH, H_U1, H_U2, H_IST, H_INVT, H_N = 12 };
+enum { H_SCALE, H_WG, H_MTW, H_MEW, H_GQ12, H_WH, H_U1, H_U2, H_IST, H_INVT, H_F3, H_N = 12 };
 constexpr int HD = TAB;              // header offset inside a slot
 constexpr int SLOT = TAB + H_N;      // doubles per table slot
 
@@ -275,6 +275,22 @@ template <int NT_> constexpr int red_size() { return 12 * NT_ + 16; }   // doubl
 // their totals are written and every thread waits for that phase, so warp 0
 // (which builds the heaviest table in the same window) is not part of the
 // hand-over and the row has ONE CTA-wide barrier; 0: a second __syncthreads.
+#ifndef M32_EPOW
+#define M32_EPOW 1
+#endif
+// v32: three trades of l-indexed table loads (4 shared-memory wavefronts each, the
+// L1TEX pipe being the loaded unit again after v31) against a few fp64 operations
+// or registers.  M32_EPOW: E2 W2^n (n = 1..3) formed in the thread from E2 and W2
+// (8 fp64) instead of three loads; M32_RPOW: R^2, R^4, R^8 of the Gaussian cross
+// term squared up in the thread (3 fp64) instead of two loads; M32_KEEPL: row j's
+// E2 and W2 kept in registers from the target evaluation to step 5 instead of two
+// reloads after the hand-over.  C5 micro 20.89 -> 20.70 -> 20.52 -> 20.36 ms.
+#ifndef M32_KEEPL
+#define M32_KEEPL 1
+#endif
+#ifndef M32_RPOW
+#define M32_RPOW 1
+#endif
 #ifndef M32_MBAR_B
 #define M32_MBAR_B 0
 #endif
@@ -457,6 +473,9 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
             sts2(T + HD + H_GQ12, P.gq12, P.wh);
             sts2(T + HD + H_U1, P.u1, P.u2);
             sts2(T + HD + H_IST, P.isT, P.invT);
+#if M32_EPOW
+            T[HD + H_F3] = mtw * (P.gT2 * P.invT * P.inv2T);
+#endif
         }
     } else if (t < 64) {
         const double W2 = v2s[m] - P.u2;
@@ -470,9 +489,11 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         L[L_H2 * NV] = 0.5 * w2 * w2;
 #endif
         L[L_W2 * NV] = W2;
+#if !M32_EPOW
         L[L_EW1 * NV] = E2 * W2;
         L[L_EW2 * NV] = E2 * W2s;
         L[L_EW3 * NV] = (mtw * (P.gT2 * P.invT * P.inv2T)) * (E2 * (W2s * W2));
+#endif
     } else if (gauss && t < 96) {
         // (GA, the Gaussian's k factor, is built by warp 3: this warp also reduces and
         // converts the x sums, and the row time follows the busiest warp -- moving
@@ -485,10 +506,12 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         if (m < 16) {
             X[X_X0R + 2 * lp] = x;
         } else {
-            const double r2 = x * x, r4 = r2 * r2;
             X[X_X0R + 2 * lp + 1] = x;
+#if !M32_RPOW
+            const double r2 = x * x, r4 = r2 * r2;
             sts2(X + X_R24 + 2 * lp, r2, r4);
             X[X_R8 + lp] = r4 * r4;
+#endif
         }
     } else {
         // the exp-free K-table pairs (off warp 0's critical path)
@@ -1251,14 +1274,39 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                                 : (ST ? nullptr : (j == 0 ? wb : (j == g.by - 1 ? wt : nullptr)));
         // acc = wh g^ + wg (G* - dt Z_y): everything of G^{n+1}(j) but the
         // y-projection, which waits for this reduction
+#if M32_KEEPL
+        double2 E2j = make_double2(0.0, 0.0), W2j = make_double2(0.0, 0.0);   // row j's l factors, kept for step 5
+#endif
         if (row_j) {
             const double* T = T0;
             const double wg = T[HD + H_WG];
+#if M32_KEEPL
+            E2j = lds2(T + LT + L_E2 * NV + lb);
+            W2j = lds2(T + LT + L_W2 * NV + lb);
+#endif
             if (wsrc == nullptr) {
+#if M32_KEEPL
+                const double2 E2 = E2j;
+#else
                 const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
+#endif
+#if M32_EPOW
+                // E2 W2^n from E2 and W2 in the thread (8 fp64) instead of three
+                // more 16-byte table loads (the l-indexed loads cost 4 wavefronts each)
+#if M32_KEEPL
+                const double2 W2t = W2j;
+#else
+                const double2 W2t = lds2(T + LT + L_W2 * NV + lb);
+#endif
+                const double f3s = T[HD + H_F3];
+                const double2 e1 = make_double2(E2.x * W2t.x, E2.y * W2t.y);
+                const double2 e2 = make_double2(e1.x * W2t.x, e1.y * W2t.y);
+                const double2 e3 = make_double2(f3s * (e2.x * W2t.x), f3s * (e2.y * W2t.y));
+#else
                 const double2 e1 = lds2(T + LT + L_EW1 * NV + lb);
                 const double2 e2 = lds2(T + LT + L_EW2 * NV + lb);
                 const double2 e3 = lds2(T + LT + L_EW3 * NV + lb);
+#endif
                 // ES-BGK Gaussian GA GB X with X(k, l) = exp(q12 W1 W2): the
                 // thread's base X0 R^kb from the cross-term table, then R^8 per pair
                 double2 GB = make_double2(0.0, 0.0);
@@ -1268,8 +1316,17 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                 if (gauss) {
                     GB = lds2(T + GL + lb);
                     const double2 x0 = lds2(T + XT + X_X0R + xsel);   // X0, R
+#if M32_RPOW
+                    // R^2, R^4, R^8 squared up in the thread (3 fp64) instead of
+                    // two more table loads
+                    double2 r24;
+                    r24.x = x0.y * x0.y;
+                    r24.y = r24.x * r24.x;
+                    const double r8 = r24.y * r24.y;
+#else
                     const double2 r24 = lds2(T + XT + X_R24 + xsel);  // R^2, R^4
                     const double r8 = T[XT + X_R8 + lp];
+#endif
                     const double xb = (x0.x * ((kb & 1) ? x0.y : 1.0)) *
                                       (((kb & 2) ? r24.x : 1.0) * ((kb & 4) ? r24.y : 1.0));
                     const double r16 = r8 * r8;
@@ -1335,8 +1392,12 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
             // G^{n+1} = acc + wg Zhat_y, Zhat_y = (a1 + w1 a2 + h1 a4 + w2 a3 + h2 a4) M
             // split as (al pE1) E2 + pE1 (b E2) with wg folded into the a's
             const double* T = T0;
+#if M32_KEEPL
+            const double2 E2 = E2j, W2 = W2j;
+#else
             const double2 E2 = lds2(T + LT + L_E2 * NV + lb);
             const double2 W2 = lds2(T + LT + L_W2 * NV + lb);
+#endif
 #if M32_TABPROJ
             const double2 bEy = lds2(T + LT + L_BEY * NV + lb);
             const double bE0 = bEy.x, bE1 = bEy.y;
