@@ -31,7 +31,7 @@
 // version of this kernel: bump on every change that alters its code, so
 // committed ncu captures (profiles/micro_traffic.json) stay tied to it
 #ifndef M32_KERNEL_VERSION
-#define M32_KERNEL_VERSION 32
+#define M32_KERNEL_VERSION 33
 #endif
 
 // Projection sums in raw velocity moments (v28).  1: each thread weights its
@@ -188,7 +188,7 @@ __device__ __forceinline__ void reduce16(double (&v)[16], double* sred) {
 
 // Row header stored in each table slot (doubles): per-cell scalars the node
 // loops need, so they come from shared memory instead of global loads.
-enum { H_SCALE, H_WG, H_MTW, H_MEW, H_GQ12, H_WH, H_U1, H_U2, H_IST, H_INVT, H_F3, H_N = 12 };
+enum { H_SCALE, H_WG, H_MTW, H_MEW, H_GQ12, H_WH, H_U1, H_U2, H_IST, H_INVT, H_N = 12 };
 constexpr int HD = TAB;              // header offset inside a slot
 constexpr int SLOT = TAB + H_N;      // doubles per table slot
 
@@ -463,7 +463,13 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
         // f0 = U, f1 = (W1 s12 + q1 gT2) / T, f2 = (p1 - s11) / (2T), f3 = gT2 / (2T^2)
         sts2(K + K_F0, pe * fma(mtw, U, gauss ? -a.inveps * P.wh : 0.0),
              pe * (mtw * ((W1 * P.s12 + q1 * P.gT2) * P.invT)));
+#if M32_EPOW
+        // (pE1 f2, pE1 f3): the thread forms E2 W2^3 itself, so f3 rides with pE1 here
+        sts2(K + K_F2, pe * (mtw * ((p1 - P.s11) * P.inv2T)),
+             pe * (mtw * (P.gT2 * P.invT * P.inv2T)));
+#else
         sts2(K + K_F2, pe * (mtw * ((p1 - P.s11) * P.inv2T)), pe);   // pE1 again: one 16-byte load in the target
+#endif
 #if M32_TABPROJ
         K[K_PEX] = pe;
 #endif
@@ -473,9 +479,6 @@ __device__ __forceinline__ void build_tables(const MicroArgs& a, double* T, cons
             sts2(T + HD + H_GQ12, P.gq12, P.wh);
             sts2(T + HD + H_U1, P.u1, P.u2);
             sts2(T + HD + H_IST, P.isT, P.invT);
-#if M32_EPOW
-            T[HD + H_F3] = mtw * (P.gT2 * P.invT * P.inv2T);
-#endif
         }
     } else if (t < 64) {
         const double W2 = v2s[m] - P.u2;
@@ -1298,10 +1301,9 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
 #else
                 const double2 W2t = lds2(T + LT + L_W2 * NV + lb);
 #endif
-                const double f3s = T[HD + H_F3];
                 const double2 e1 = make_double2(E2.x * W2t.x, E2.y * W2t.y);
                 const double2 e2 = make_double2(e1.x * W2t.x, e1.y * W2t.y);
-                const double2 e3 = make_double2(f3s * (e2.x * W2t.x), f3s * (e2.y * W2t.y));
+                const double2 e3 = make_double2(e2.x * W2t.x, e2.y * W2t.y);   // (f3 is in the K-table entry)
 #else
                 const double2 e1 = lds2(T + LT + L_EW1 * NV + lb);
                 const double2 e2 = lds2(T + LT + L_EW2 * NV + lb);
@@ -1341,7 +1343,7 @@ __global__ void __launch_bounds__(512 / NP_, MICRO32_MINB) k_micro32(MicroArgs a
                     // closed-form target (_core.pyx:220-224), factored and
                     // pre-scaled by -wh/tau (minus wh/eps when Gaussian)
                     const double2 f01 = lds2(K + K_F0);   // pe f0', pe f1'
-                    const double2 f2p = lds2(K + K_F2);   // pe f2', pe
+                    const double2 f2p = lds2(K + K_F2);   // pe f2', pe f3' (pe itself without M32_EPOW)
                     const double f2 = f2p.x, pe = f2p.y;
                     double P0 = fma(wg, ty[2 * p], f01.x * E2.x);
                     double P1 = fma(wg, ty[2 * p + 1], f01.x * E2.y);
